@@ -1,0 +1,238 @@
+/*
+ * eco_b200.h — C ABI of the B200 eco-driving DP solver.
+ *
+ * Plain C: POD structs, raw pointers and sizes, integer status codes, no
+ * exceptions and no torch types.  Every entry point replaces one call site
+ * of the reference package `ecodrive` (paths relative to
+ * /root/reference/pkg/src/ecodrive/):
+ *
+ *   eco_bellman_step   <- backward_step           dp.py:365-404
+ *                         (= _kernels.dp_sweep_serial _kernels.py:421-546,
+ *                          = parallel_step           parallel.py:152-158;
+ *                          tables != NULL is the use_tables / toy_mode path
+ *                          of _kernels.py:476-493 and solve_toy dp.py:557-610)
+ *   eco_solve_horizon  <- solve_horizon           dp.py:425-475
+ *   eco_field_build    <- build_terminal_cost     mpc.py:96-158
+ *                         (loop of _kernels.field_sweep _kernels.py:801-865)
+ *   eco_mpc_run        <- EcoDrivingMPC.fit + simulate_closed_loop
+ *                                                  mpc.py:379-391, 513-596
+ *   eco_solve_batch    <- run_bench inner loop    bench.py:136-148
+ *                         (many independent solve_horizon calls)
+ *
+ * Conventions (dp.py:383-384, _kernels.py:540-545): infeasible cost-to-go is
+ * exactly j_inf, infeasible policy entries are -1, policy values are flat
+ * action indices ite * n_tb + itb.  All host arrays are C-contiguous,
+ * row-major (v, soc, t) with t fastest.  Outputs are written by the callee.
+ *
+ * Precision: ECO_FP64 computes the value path in IEEE double with unfused
+ * arithmetic (bitwise equal to the reference); ECO_FP32 keeps the transition
+ * geometry in double and the cost-to-go gather / argmin in float.
+ */
+#ifndef ECO_B200_H
+#define ECO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECO_ABI_VERSION 1
+
+#define ECO_MAX_GEARS 16
+#define ECO_MAX_AXIS 32
+#define ECO_MAX_MAP (ECO_MAX_AXIS * ECO_MAX_AXIS)
+#define ECO_MAX_WINDOWS 8
+
+/* status codes */
+#define ECO_OK 0
+#define ECO_ERR_ARG 1      /* invalid argument (sizes, null pointers) */
+#define ECO_ERR_CUDA 2     /* CUDA runtime failure; see eco_last_error() */
+#define ECO_ERR_NODEV 3    /* no CUDA device visible */
+
+/* precision selector */
+#define ECO_FP32 0
+#define ECO_FP64 1
+
+/* node kinds (route.py:29-31) */
+#define ECO_NODE_PLAIN 0
+#define ECO_NODE_SIGNAL 1
+#define ECO_NODE_STOP 2
+
+/* Packed plant: the fields of PlantPack (_kernels.py:31-53) with fixed-capacity
+ * arrays.  shift_v holds n_gears - 1 entries; maps are row-major. */
+typedef struct EcoPlant {
+    double mass, c0, c1, c2, wheel_radius, final_drive;
+    double idle_speed, belt_ratio;
+    double r0, c_nom, soc_min, soc_max, p_bat_max;
+    int32_t n_gears, n_eng, n_fuel_w, n_fuel_t;
+    int32_t n_bsg, n_eff_w, n_eff_t, n_voc;
+    double gear_ratios[ECO_MAX_GEARS];
+    double gear_eff[ECO_MAX_GEARS];
+    double shift_v[ECO_MAX_GEARS];
+    double eng_w[ECO_MAX_AXIS], eng_tmin[ECO_MAX_AXIS], eng_tmax[ECO_MAX_AXIS];
+    double fuel_w[ECO_MAX_AXIS], fuel_t[ECO_MAX_AXIS];
+    double bsg_w[ECO_MAX_AXIS], bsg_tmin[ECO_MAX_AXIS], bsg_tmax[ECO_MAX_AXIS];
+    double eff_w[ECO_MAX_AXIS], eff_t[ECO_MAX_AXIS];
+    double voc_soc[ECO_MAX_AXIS], voc_v[ECO_MAX_AXIS];
+    double fuel_vals[ECO_MAX_MAP];
+    double eff_vals[ECO_MAX_MAP];
+} EcoPlant;
+
+/* Grid and per-solve scalars shared by every step (GridSpec dp.py:41-83,
+ * SolveContext dp.py:191-214, PenaltyConfig dp.py:86-98). */
+typedef struct EcoProblem {
+    int32_t n_v, n_soc, n_t, n_te, n_tb;
+    int32_t reserved;
+    double delta_d, a_min, a_max;   /* route spacing and comfort box */
+    double gamma, j_inf;
+    double t0, dtg;                  /* time ladder t_z = t_axis[z], spacing */
+    const double* te_axis;           /* n_te */
+    const double* tb_axis;           /* n_tb */
+    const double* soc_axis;          /* n_soc */
+    const double* t_axis;            /* n_t */
+} EcoProblem;
+
+/* One spatial step m -> m+1 (StepPlan dp.py:173-188). */
+typedef struct EcoStepPlan {
+    int32_t node, src_kind, dest_kind, reserved;
+    double grade, v0_dest, dv_dest;
+    double cos_grade, sin_grade;  /* host libm cos/sin(grade): road_load K:134-142 */
+    const double* v_src;      /* n_v source speed axis */
+    const uint8_t* arr_green; /* n_t destination green mask */
+    const uint8_t* dep_ok;    /* n_t source standstill departure allowed */
+    const double* t_dep;      /* n_t */
+    const double* wait;       /* n_t */
+} EcoStepPlan;
+
+/* Table-driven (v, u) transition quantities, shape (n_v, n_te, n_tb) each:
+ * the s1* arguments of dp_sweep_serial (_kernels.py:424), used by toy
+ * instances (dp.py:482-610). */
+typedef struct EcoStage1Tables {
+    const uint8_t* ok;
+    const double* v2;
+    const double* dt;
+    const double* pbat;
+    const double* c1;
+    const int32_t* ivlo;
+    const int32_t* ivhi;
+    const double* wv;
+    const int32_t* zoff;
+    const double* wz;
+} EcoStage1Tables;
+
+/* Route with SPaT (Route route.py:102-184, SignalTiming route.py:34-86). */
+typedef struct EcoRoute {
+    int32_t node_count;
+    int32_t reserved;
+    double delta_d, accel_min, accel_max, stop_dwell;
+    const double* v_min;      /* node_count */
+    const double* v_max;      /* node_count */
+    const double* grade;      /* node_count */
+    const double* cos_grade;  /* node_count, host libm cos(grade) */
+    const double* sin_grade;  /* node_count, host libm sin(grade) */
+    const int8_t* kinds;      /* node_count, ECO_NODE_* */
+    /* per node (meaningful where kinds == ECO_NODE_SIGNAL) */
+    const double* sig_cycle;  /* node_count */
+    const double* sig_offset; /* node_count */
+    const int32_t* sig_nwin;  /* node_count */
+    const double* sig_win;    /* node_count * ECO_MAX_WINDOWS * 2 ([start,end)) */
+} EcoRoute;
+
+/* Controller settings (EcoDrivingMPC.__init__ mpc.py:354-377). */
+typedef struct EcoMpcConfig {
+    int32_t n_v, n_soc, n_t, n_te, n_tb;
+    int32_t horizon;
+    int32_t teleport;             /* 1: red wait allowed (default) */
+    int32_t use_terminal_field;   /* 1: offline field (default) */
+    int32_t precision;            /* ECO_FP32 / ECO_FP64 */
+    int32_t start_node;           /* closed loop starts at this node (0 = route start) */
+    int32_t max_steps;            /* < 0: drive to the end of the route */
+    int32_t reserved;
+    double dt;                    /* ladder spacing */
+    double gamma, soc_target, soc_weight, j_inf;
+    const double* te_axis;        /* n_te */
+    const double* tb_axis;        /* n_tb */
+} EcoMpcConfig;
+
+/* One closed-loop step (TrajectoryStep mpc.py:418-435). */
+typedef struct EcoTrajRow {
+    int32_t s, gear, fallback, horizon;
+    double v, soc, t, t_eng, t_bsg, brake_force;
+    double wait_s, dt_move_s, fuel_inc_g, accel, cost_to_go;
+} EcoTrajRow;
+
+/* Diagnostics returned by the solvers. */
+typedef struct EcoStats {
+    double device_ms;          /* CUDA-event time of the device work */
+    double dominant_ms;        /* CUDA-event time of the Bellman sweeps only */
+    int64_t dense_updates;     /* N_s * n_te * n_tb * stages */
+    int64_t live_updates;      /* candidates that reached the value gather (counted when requested) */
+    int64_t stages;            /* Bellman stages executed */
+    int64_t kernel_launches;   /* kernels launched by this call */
+} EcoStats;
+
+/* closed-loop status codes */
+#define ECO_RUN_OK 0
+#define ECO_RUN_INFEASIBLE 1   /* no admissible action and max-brake impossible */
+#define ECO_RUN_PLANT 2        /* plant step raised (zero mean velocity, power, rule) */
+
+int32_t eco_abi_version(void);
+const char* eco_last_error(void);
+int32_t eco_device_count(void);
+
+/* One backward Bellman step (backward_step, dp.py:365-404).  J_next, J_out
+ * are (n_v, n_soc, n_t) f64, P_out int32.  tables may be NULL (plant path). */
+int32_t eco_bellman_step(const EcoPlant* plant, const EcoProblem* prob,
+                         const EcoStepPlan* plan, const EcoStage1Tables* tables,
+                         const double* J_next, double* J_out, int32_t* P_out,
+                         int32_t precision, int32_t count_live, EcoStats* stats);
+
+/* Whole-horizon backward recursion (solve_horizon, dp.py:425-475).
+ * plans[0..H-1]; terminal (n_v, n_soc, n_t); J_stack (H+1) levels with
+ * index 0 = start node; P_stack H levels. */
+int32_t eco_solve_horizon(const EcoPlant* plant, const EcoProblem* prob,
+                          const EcoStepPlan* plans, int32_t H,
+                          const double* terminal, double* J_stack,
+                          int32_t* P_stack, int32_t precision,
+                          int32_t count_live, EcoStats* stats);
+
+/* Table-driven horizon solve (solve_toy, dp.py:557-610): tables[k] holds the
+ * (n_v, n_te, n_tb) transition quantities of step k; battery power is read per
+ * action (toy_mode of dp_stage2_sweep, _kernels.py:676-683). */
+int32_t eco_solve_tables(const EcoPlant* plant, const EcoProblem* prob,
+                         const EcoStepPlan* plans, const EcoStage1Tables* tables,
+                         int32_t H, const double* terminal, double* J_stack,
+                         int32_t* P_stack, int32_t precision);
+
+/* Offline terminal field (build_terminal_cost, mpc.py:96-158):
+ * field_out (node_count, n_v, n_soc) f64. */
+int32_t eco_field_build(const EcoPlant* plant, const EcoRoute* route,
+                        const EcoMpcConfig* cfg, double* field_out,
+                        EcoStats* stats);
+
+/* Closed loop (EcoDrivingMPC.fit + simulate_closed_loop, mpc.py:379-596) on
+ * the device.  rows has room for node_count - 1 entries; *n_rows receives the
+ * number of steps taken, *status an ECO_RUN_* code, final_state (v, soc, t).
+ * field_in may hold a precomputed field (node_count, n_v, n_soc); when NULL
+ * and cfg->use_terminal_field, the field is built on the device first.
+ * field_out (nullable) receives the field used. */
+int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route,
+                    const EcoMpcConfig* cfg, const double* x_start,
+                    const double* field_in, double* field_out,
+                    EcoTrajRow* rows, int32_t* n_rows, int32_t* status,
+                    int32_t* status_node, double* final_state, EcoStats* stats);
+
+/* Batch of independent horizon solves sharing one route geometry (C4):
+ * scenario i starts at node s[i], time t_start[i] with its own SPaT
+ * (routes[i]).  Writes the start-node cost-to-go J0 (n_scen, n_v, n_soc, n_t)
+ * and its policy P0 when the pointers are non-NULL. */
+int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* routes,
+                        int32_t n_scen, const int32_t* s, const double* t_start,
+                        const EcoMpcConfig* cfg, double* J0, int32_t* P0,
+                        EcoStats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECO_B200_H */

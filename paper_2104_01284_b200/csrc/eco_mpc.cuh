@@ -1,0 +1,303 @@
+// eco_mpc.cuh — device-resident receding-horizon loop pieces.
+//
+//   prepare  <- build_context        dp.py:255-341  (ladders, terminal seed)
+//   decide   <- _argmin_at_state     mpc.py:189-278
+//              + _max_braking_decision mpc.py:490-510
+//              + propagate_state_full  plant.py:341-439
+//              + simulate_closed_loop  mpc.py:549-594 (row log, mismatch check)
+//
+// The state x = (v, soc, t) never leaves the device during a run; one
+// prepare / h stage sweeps / one decide launch per route node.
+#pragma once
+
+#include "eco_kernels.cuh"
+
+namespace eco {
+
+struct DevRoute {               // device copies of EcoRoute arrays
+    int n;
+    double delta_d, accel_min, accel_max, stop_dwell;
+    const double* v_min;
+    const double* v_max;
+    const double* grade;
+    const double* cos_g;
+    const double* sin_g;
+    const int8_t* kinds;
+    const double* sig_cycle;
+    const double* sig_offset;
+    const int32_t* sig_nwin;
+    const double* sig_win;
+};
+
+struct LoopState {              // lives in device memory for the whole run
+    double x[3];                // v, soc, t
+    int32_t status;             // ECO_RUN_* (3 = prediction mismatch)
+    int32_t status_node;
+    int32_t n_rows;
+    int32_t pad;
+};
+
+struct Ladders {                // [H+1][nt] per receding-horizon solve
+    uint8_t* green;
+    uint8_t* dep_ok;
+    double* t_dep;
+    double* wait;
+    double* t_axis;             // [nt]
+};
+
+struct LoopCfg {
+    int nv, nx, nt, nte, ntb, U, H, teleport, use_field;
+    double dt, gamma, soc_target, soc_weight, j_inf;
+    const double* te_axis;
+    const double* tb_axis;
+    const double* soc_axis;     // [nx]
+    const double* vaxes;        // [n][nv] node speed axes
+};
+
+// _node_time_arrays dp.py:217-252 for one node on the ladder
+__device__ __forceinline__ void node_ladder(const DevRoute& r, int node, const double* t_axis, int nt, int teleport,
+                                            uint8_t* green, uint8_t* dep, double* tdep, double* wait, int z) {
+    const double tz = t_axis[z];
+    uint8_t g = 1, d = 1;
+    double td = tz, w = 0.0;
+    const int kind = r.kinds[node];
+    if (kind == ECO_NODE_SIGNAL) {
+        const double* win = r.sig_win + (size_t)node * ECO_MAX_WINDOWS * 2;
+        if (!sig_is_green(r.sig_cycle[node], r.sig_offset[node], win, r.sig_nwin[node], tz)) {
+            g = 0;
+            if (teleport) {
+                const double ng = sig_next_green(r.sig_cycle[node], r.sig_offset[node], win, r.sig_nwin[node], tz);
+                td = ng;
+                w = ng - tz;
+            } else {
+                d = 0;
+            }
+        }
+    } else if (kind == ECO_NODE_STOP) {
+        td = tz + r.stop_dwell;
+        w = r.stop_dwell;
+    }
+    green[z] = g; dep[z] = d; tdep[z] = td; wait[z] = w;
+}
+
+// terminal seed dp.py:322-334: min(base + w*(xi - xi*)^2, j_inf), j_inf where
+// base >= j_inf, constant along t; written in the internal (+inf) form.
+template <typename Real>
+__device__ __forceinline__ Real terminal_value(double base, double soc, double target, double weight, double j_inf) {
+    const double d = soc - target;
+    const double q = weight * (d * d);
+    double val;
+    if (base >= j_inf) val = j_inf;
+    else { val = base + q; if (!(val < j_inf)) val = j_inf; }
+    return val >= j_inf ? (Real)INFINITY : (Real)val;
+}
+
+// One block.  Builds the time ladder at x.t, the node ladders of nodes
+// s..s+h and the terminal level J_h.
+template <typename Real>
+__global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, int s, int h,
+                                   const double* field, Ladders lad, Real* Jh) {
+    if (st->status != 0) return;
+    __shared__ double t_axis[1024];
+    const double t = st->x[2];
+    const double t0 = c.dt * floor(t / c.dt);          // GridSpec.t_axis dp.py:75-77
+    for (int z = threadIdx.x; z < c.nt; z += blockDim.x) {
+        const double tz = t0 + c.dt * (double)z;
+        lad.t_axis[z] = tz;
+        if (z < 1024) t_axis[z] = tz;
+    }
+    __syncthreads();
+    const double* tax = c.nt <= 1024 ? t_axis : lad.t_axis;
+    for (int i = threadIdx.x; i < (h + 1) * c.nt; i += blockDim.x) {
+        const int k = i / c.nt, z = i - k * c.nt;
+        node_ladder(r, s + k, tax, c.nt, c.teleport, lad.green + (size_t)k * c.nt, lad.dep_ok + (size_t)k * c.nt,
+                    lad.t_dep + (size_t)k * c.nt, lad.wait + (size_t)k * c.nt, z);
+    }
+    const size_t plane = (size_t)c.nx * c.nt;
+    for (size_t i = threadIdx.x; i < (size_t)c.nv * plane; i += blockDim.x) {
+        const int iv = (int)(i / plane);
+        const int jx = (int)((i - iv * plane) / c.nt);
+        const double base = (c.use_field && field) ? field[((size_t)(s + h) * c.nv + iv) * c.nx + jx] : 0.0;
+        Jh[i] = terminal_value<Real>(base, c.soc_axis[jx], c.soc_target, c.soc_weight, c.j_inf);
+    }
+}
+
+// interp3_abs (K:340-361) on an internal table at a continuous query,
+// CostToGoTable.interpolate dp.py:115-134: returns j_inf when infeasible.
+template <typename Real>
+__device__ double table_interp(const Real* J, const double* va, int nv, const double* xa, int nx,
+                               const double* ta, int nt, double j_inf, double v, double x, double t) {
+    const double v0 = va[0], dv = (va[nv - 1] - v0) / (nv - 1);
+    const double x0 = xa[0], dx = (xa[nx - 1] - x0) / (nx - 1);
+    const double t0 = ta[0], dtg = (ta[nt - 1] - t0) / (nt - 1);
+    int a0, a1, b0, b1, c0, c1;
+    double wa, wb, wc;
+    const bool ok = locate_uniform(v, v0, dv, nv, &a0, &a1, &wa) && locate_uniform(x, x0, dx, nx, &b0, &b1, &wb) &&
+                    locate_uniform(t, t0, dtg, nt, &c0, &c1, &wc);
+    if (!ok) return j_inf;
+    auto at = [&](int i, int j, int k) -> double {
+        const Real r = J[((size_t)i * nx + j) * nt + k];
+        return r;  // +inf stays +inf
+    };
+    auto bil = [&](int k) -> double {
+        const double c00 = at(a0, b0, k), c01 = at(a0, b1, k), c10 = at(a1, b0, k), c11 = at(a1, b1, k);
+        if (c00 >= j_inf || c01 >= j_inf || c10 >= j_inf || c11 >= j_inf) return j_inf;
+        const double lo = c00 + wa * (c10 - c00);
+        const double hi = c01 + wa * (c11 - c01);
+        return lo + wb * (hi - lo);
+    };
+    const double r0 = bil(c0);
+    if (r0 >= j_inf) return j_inf;
+    if (c1 == c0) return r0;
+    const double r1 = bil(c1);
+    if (r1 >= j_inf) return j_inf;
+    return r0 + wc * (r1 - r0);
+}
+
+constexpr int kDecideThreads = 1024;
+
+// One block of kDecideThreads.  argmin over the action grid at the exact
+// state on level J_1 (the solve's tables[1]), then the plant step.
+template <typename Real>
+__global__ void __launch_bounds__(kDecideThreads)
+mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
+                  Ladders lad, const Real* J1, EcoTrajRow* rows) {
+    if (st->status != 0) return;
+    const EcoPlant& P = *plant;
+    __shared__ double s_f[kDecideThreads / 32];
+    __shared__ int s_u[kDecideThreads / 32];
+    __shared__ double s_wait, s_tbase;
+    __shared__ int s_src_ok;
+    const double v = st->x[0], soc = st->x[1], t = st->x[2];
+    const int src = r.kinds[s], dst = r.kinds[s + 1];
+    if (threadIdx.x == 0) {
+        double wait = 0.0, t_base = t;
+        int ok = 1;
+        if (src == ECO_NODE_STOP) {
+            if (v > 0.0) ok = 0;
+            wait = r.stop_dwell;
+            t_base = t + wait;
+        } else if (src == ECO_NODE_SIGNAL && v == 0.0) {
+            const double* win = r.sig_win + (size_t)s * ECO_MAX_WINDOWS * 2;
+            if (!sig_is_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t)) {
+                if (!c.teleport) ok = 0;
+                t_base = sig_next_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t);
+                wait = t_base - t;
+            }
+        }
+        s_wait = wait; s_tbase = t_base; s_src_ok = ok;
+    }
+    __syncthreads();
+    const double wait = s_wait, t_base = s_tbase;
+    const StepPre q = step_pre(P, v, r.cos_g[s], r.sin_g[s]);
+    const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
+    double bestf = 0.0;
+    int bestu = -1;
+    if (s_src_ok) {
+        for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
+            const int ite = u / c.ntb, itb = u - ite * c.ntb;
+            const double te = c.te_axis[ite], tb = c.tb_axis[itb];
+            if (te > q.te_hi || te < q.te_lo || tb > q.tb_hi || tb < q.tb_lo) continue;
+            const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, r.accel_min, r.accel_max, 0.0, q);
+            if (o.feas != kFeasOk) continue;
+            if (o.clamped && dst == ECO_NODE_PLAIN) continue;
+            if (dst == ECO_NODE_STOP && o.v_next > 0.0) continue;
+            double cur;
+            if (!battery_current(P, o.p_bat, soc, &cur)) continue;
+            const double soc2 = soc - o.dt_move * cur / P.c_nom;
+            const double t2 = t_base + o.dt_move;
+            if (o.v_next > 0.0) {            // floor-sample green gate mpc.py:256-261
+                int zlo, zhi;
+                double w;
+                if (locate_uniform(t2, lad.t_axis[0], c.dt, c.nt, &zlo, &zhi, &w) && lad.green[c.nt + zlo] == 0)
+                    continue;
+            }
+            const double jn = table_interp<Real>(J1, v1, c.nv, c.soc_axis, c.nx, lad.t_axis, c.nt, c.j_inf,
+                                                 o.v_next, soc2, t2);
+            if (!(jn < c.j_inf)) continue;
+            const double f = stage_cost(o.mf, o.dt_move, c.gamma) + (1.0 - c.gamma) * wait + jn;
+            if (bestu < 0 || f < bestf) { bestf = f; bestu = u; }
+        }
+    }
+    // lexicographic (f, u) min == first win in scan order (mpc.py:269)
+    for (int o = 16; o > 0; o >>= 1) {
+        const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
+        const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
+        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) { bestf = f2; bestu = u2; }
+    }
+    if ((threadIdx.x & 31) == 0) { s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        const int u2 = s_u[w];
+        const double f2 = s_f[w];
+        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) { bestf = f2; bestu = u2; }
+    }
+    EcoTrajRow row{};
+    row.s = s; row.v = v; row.soc = soc; row.t = t; row.horizon = h;
+    double te = 0.0, tb = 0.0, brake = 0.0;
+    double pred[3] = {0.0, 0.0, 0.0};
+    if (bestu >= 0) {
+        te = c.te_axis[bestu / c.ntb];
+        tb = c.tb_axis[bestu % c.ntb];
+        row.cost_to_go = bestf;
+        // re-evaluate the winner for the predicted state (same arithmetic)
+        const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, r.accel_min, r.accel_max, 0.0, q);
+        double cur;
+        battery_current(P, o.p_bat, soc, &cur);
+        pred[0] = o.v_next;
+        pred[1] = soc - o.dt_move * cur / P.c_nom;
+        pred[2] = t_base + o.dt_move;
+    } else {
+        // _max_braking_decision mpc.py:490-510
+        if (v <= 0.0) { st->status = ECO_RUN_INFEASIBLE; st->status_node = s; return; }
+        double a_target;
+        if (dst == ECO_NODE_PLAIN) {
+            const double a_stop = -(v * v) / (2.0 * r.delta_d) * (1.0 - 1.0e-2);
+            a_target = r.accel_min >= a_stop ? r.accel_min : a_stop;
+        } else {
+            a_target = r.accel_min;
+        }
+        const double f_road = road_load(P, v, r.cos_g[s], r.sin_g[s]);
+        const double b = -(P.mass * a_target + f_road);
+        brake = b > 0.0 ? b : 0.0;
+        row.cost_to_go = __longlong_as_double(0x7ff8000000000000ULL);   // NaN (ControlDecision default)
+        row.fallback = 1;
+    }
+    // propagate_state_full plant.py:341-439
+    if (!(q.te_lo <= te && te <= q.te_hi) || !(q.tb_lo <= tb && tb <= q.tb_hi) || brake < 0.0) {
+        st->status = ECO_RUN_PLANT; st->status_node = s; return;
+    }
+    double wait_p = 0.0, tb_p = t;
+    if (v == 0.0) {
+        if (src == ECO_NODE_SIGNAL) {
+            const double* win = r.sig_win + (size_t)s * ECO_MAX_WINDOWS * 2;
+            if (!sig_is_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t)) {
+                if (!c.teleport) { st->status = ECO_RUN_PLANT; st->status_node = s; return; }
+                tb_p = sig_next_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t);
+                wait_p = tb_p - t;
+            }
+        } else if (src == ECO_NODE_STOP) {
+            wait_p = r.stop_dwell;
+            tb_p = t + wait_p;
+        }
+    }
+    const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, -INFINITY, INFINITY, brake, q);
+    if (o.feas == kFeasNoMotion || (o.clamped && dst == ECO_NODE_PLAIN) || (dst == ECO_NODE_STOP && o.v_next > 0.0)) {
+        st->status = ECO_RUN_PLANT; st->status_node = s; return;
+    }
+    double cur;
+    if (!battery_current(P, o.p_bat, soc, &cur)) { st->status = ECO_RUN_PLANT; st->status_node = s; return; }
+    const double nx0 = o.v_next, nx1 = soc - o.dt_move * cur / P.c_nom, nx2 = tb_p + o.dt_move;
+    if (bestu >= 0 && !(pred[0] == nx0 && pred[1] == nx1 && pred[2] == nx2)) {
+        st->status = 3; st->status_node = s; return;                     // mpc.py:575-582
+    }
+    row.t_eng = te; row.t_bsg = tb; row.brake_force = brake;
+    row.gear = q.d.gear;
+    row.wait_s = wait_p; row.dt_move_s = o.dt_move; row.fuel_inc_g = o.mf * o.dt_move; row.accel = o.accel;
+    rows[st->n_rows] = row;
+    st->n_rows += 1;
+    st->x[0] = nx0; st->x[1] = nx1; st->x[2] = nx2;
+}
+
+}  // namespace eco

@@ -1,0 +1,332 @@
+"""Receding-horizon eco-driving controller and the device-resident closed loop.
+
+Front end with the reference's names and semantics (mpc.py:47-596):
+``TerminalCostField``, ``build_terminal_cost``, ``field_value``,
+``EcoDrivingMPC`` (fit / control), ``mpc_step``, ``simulate_closed_loop``,
+``ControlDecision``, ``TrajectoryStep``, ``ClosedLoopTrajectory``.
+
+Execution is on the B200: the offline field sweep, every horizon solve, the
+exact-state argmin, the max-brake fallback and the plant step all run in the
+sm_100a library (``eco_mpc_run``); the loop state never leaves the device
+until the trajectory is copied back once at the end.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field as dc_field
+from typing import Optional
+
+import numpy as np
+
+from . import _abi
+from .dp import (GridSpec, PenaltyConfig, locate_uniform, precision_of, _bilin_abs)
+from .errors import StartStateInfeasibleError
+from .plant import ActionVector, StateVector, Vehicle
+from .route import Route, SpatSchedule
+
+
+@dataclass(frozen=True)
+class TerminalCostField:
+    """Cost-to-destination per node on the (v, soc) grid (mpc.py:47-71)."""
+
+    values: np.ndarray           # (node_count, n_v, n_soc)
+    route_name: str
+    gamma: float
+    grids: GridSpec
+    penalty: PenaltyConfig
+
+    def node_slice(self, s: int) -> np.ndarray:
+        return self.values[s]
+
+    def __post_init__(self):
+        if self.values.ndim != 3:
+            raise ValueError("terminal field values must be (nodes, n_v, n_soc)")
+        if self.values.shape[1:] != (self.grids.n_v, self.grids.n_soc):
+            raise ValueError("terminal field shape does not match the grid spec")
+        if np.isnan(self.values).any():
+            raise ValueError("terminal field contains NaN")
+
+
+def field_value(field: TerminalCostField, vehicle: Vehicle, route: Route, s: int, v: float, soc: float) -> float:
+    """Bilinear field value at node s with absorbing j_inf (mpc.py:74-93)."""
+    g = field.grids
+    va, xa = g.v_axis(route, s), g.soc_axis(vehicle)
+    v0, x0 = float(va[0]), float(xa[0])
+    a0, a1, wa, oka = locate_uniform(v, v0, (float(va[-1]) - v0) / (g.n_v - 1), g.n_v)
+    b0, b1, wb, okb = locate_uniform(soc, x0, (float(xa[-1]) - x0) / (g.n_soc - 1), g.n_soc)
+    if not (oka and okb):
+        return field.penalty.j_inf
+    G = field.values[s]
+    return float(_bilin_abs(float(G[a0, b0]), float(G[a0, b1]), float(G[a1, b0]), float(G[a1, b1]),
+                            wa, wb, field.penalty.j_inf))
+
+
+def _config(vehicle, grids: GridSpec, penalty: PenaltyConfig, gamma: float, horizon: int, teleport: bool,
+            use_field: bool, backend: str, start_node: int = 0, max_steps: int = -1):
+    te, tb = grids.te_axis(), grids.tb_axis()
+    cfg = _abi.EcoMpcConfig(
+        n_v=grids.n_v, n_soc=grids.n_soc, n_t=grids.n_t, n_te=te.size, n_tb=tb.size, horizon=horizon,
+        teleport=int(teleport), use_terminal_field=int(use_field), precision=precision_of(backend),
+        start_node=start_node, max_steps=max_steps, dt=float(grids.dt), gamma=float(gamma),
+        soc_target=float(penalty.soc_target), soc_weight=float(penalty.soc_weight), j_inf=float(penalty.j_inf),
+        te_axis=_abi.ptr(te, C.c_double), tb_axis=_abi.ptr(tb, C.c_double))
+    return cfg, (te, tb)
+
+
+def build_terminal_cost(route: Route, vehicle: Vehicle, *, gamma: float, grids: GridSpec,
+                        penalty: PenaltyConfig, spat: Optional[SpatSchedule] = None,
+                        backend: str = "b200", stats: Optional[dict] = None) -> TerminalCostField:
+    """Signal-free (v, soc) backward sweep over all nodes (mpc.py:96-158), on the device."""
+    if not 0.0 <= gamma <= 1.0:
+        raise ValueError("gamma must lie in [0, 1]")
+    rp = _abi.RoutePack(route, spat if spat is not None else SpatSchedule(signals={}), signals_optional=True)
+    cfg, keep = _config(vehicle, grids, penalty, gamma, 1, True, True, backend)
+    plant = _abi.pack_plant(vehicle.pack())
+    out = np.empty((route.node_count, grids.n_v, grids.n_soc))
+    st = _abi.EcoStats()
+    _abi.check(_abi.lib().eco_field_build(C.byref(plant), C.byref(rp.c), C.byref(cfg),
+                                          _abi.ptr(out, C.c_double), C.byref(st)), "eco_field_build")
+    if stats is not None:
+        stats.update(st.as_dict())
+    return TerminalCostField(values=out, route_name=route.name, gamma=gamma, grids=grids, penalty=penalty)
+
+
+@dataclass
+class ControlDecision:
+    action: ActionVector
+    brake_force: float = 0.0
+    predicted_next: Optional[StateVector] = None
+    cost_to_go: float = math.nan
+    solver_wall_s: float = 0.0
+    fallback: bool = False
+    note: str = ""
+
+
+@dataclass
+class MpcStepInfo:
+    predicted_next: StateVector
+    cost_to_go: float
+    wait: float
+    solve_wall_s: float
+    horizon: int
+
+
+@dataclass
+class TrajectoryStep:
+    """One spatial step of a run, state taken at the source node (mpc.py:418-435)."""
+
+    s: int
+    v: float
+    soc: float
+    t: float
+    t_eng: float
+    t_bsg: float
+    brake_force: float
+    gear: int
+    wait_s: float
+    dt_move_s: float
+    fuel_inc_g: float
+    accel: float
+    cost_to_go: float
+    fallback: bool
+
+
+@dataclass
+class ClosedLoopTrajectory:
+    """Step log, final state and totals of one run (mpc.py:438-487)."""
+
+    route_name: str
+    controller: str
+    backend: str
+    delta_d: float
+    x_start: StateVector
+    steps: list = dc_field(default_factory=list)
+    solver_wall_s: list = dc_field(default_factory=list)
+    final_state: Optional[StateVector] = None
+    status: str = "ok"
+    stats: dict = dc_field(default_factory=dict)
+
+    @property
+    def completed(self) -> bool:
+        return self.status == "ok"
+
+    @property
+    def n_steps(self) -> int:
+        return len(self.steps)
+
+    @property
+    def fuel_g(self) -> float:
+        return float(sum(st.fuel_inc_g for st in self.steps))
+
+    @property
+    def travel_time_s(self) -> float:
+        return 0.0 if self.final_state is None else float(self.final_state.t - self.x_start.t)
+
+    @property
+    def soc_end(self) -> float:
+        return float(self.x_start.soc if self.final_state is None else self.final_state.soc)
+
+    def distance_m(self, step_index: int) -> float:
+        return self.steps[step_index].s * self.delta_d
+
+    def timing_stats_ms(self) -> dict:
+        if not self.solver_wall_s:
+            return {"mean_ms": 0.0, "variance_ms2": 0.0, "max_ms": 0.0}
+        arr = 1.0e3 * np.asarray(self.solver_wall_s)
+        return {"mean_ms": float(arr.mean()), "variance_ms2": float(arr.var()), "max_ms": float(arr.max())}
+
+
+def _rows_to_steps(rows: np.ndarray) -> list:
+    return [TrajectoryStep(
+        s=int(r["s"]), v=float(r["v"]), soc=float(r["soc"]), t=float(r["t"]), t_eng=float(r["t_eng"]),
+        t_bsg=float(r["t_bsg"]), brake_force=float(r["brake_force"]), gear=int(r["gear"]),
+        wait_s=float(r["wait_s"]), dt_move_s=float(r["dt_move_s"]), fuel_inc_g=float(r["fuel_inc_g"]),
+        accel=float(r["accel"]), cost_to_go=float(r["cost_to_go"]), fallback=bool(r["fallback"]))
+        for r in rows]
+
+
+def run_closed_loop(vehicle: Vehicle, route: Route, spat: SpatSchedule, x_start: StateVector, *,
+                    gamma: float, grids: GridSpec, penalty: PenaltyConfig, horizon: int, backend: str,
+                    teleport: bool = True, field: Optional[TerminalCostField] = None,
+                    use_terminal_field: bool = True, start_node: int = 0, max_steps: int = -1):
+    """One call of ``eco_mpc_run``.  Returns (rows, status, status_node,
+    final_state, field_values, stats)."""
+    n = route.node_count
+    rp = _abi.RoutePack(route, spat)
+    cfg, keep = _config(vehicle, grids, penalty, gamma, horizon, teleport, use_terminal_field, backend,
+                        start_node, max_steps)
+    plant = _abi.pack_plant(vehicle.pack())
+    x0 = np.array([x_start.v, x_start.soc, x_start.t], dtype=np.float64)
+    rows = np.zeros(max(n - 1, 1), dtype=_abi.TRAJ_DTYPE)
+    fin = np.zeros(3)
+    n_rows, status, status_node = C.c_int32(0), C.c_int32(0), C.c_int32(-1)
+    field_in = None
+    field_out = None
+    if use_terminal_field:
+        if field is not None:
+            field_in = np.ascontiguousarray(field.values, dtype=np.float64)
+        else:
+            field_out = np.empty((n, grids.n_v, grids.n_soc))
+    st = _abi.EcoStats()
+    _abi.check(_abi.lib().eco_mpc_run(
+        C.byref(plant), C.byref(rp.c), C.byref(cfg), _abi.ptr(x0, C.c_double),
+        None if field_in is None else _abi.ptr(field_in, C.c_double),
+        None if field_out is None else _abi.ptr(field_out, C.c_double),
+        rows.ctypes.data_as(C.POINTER(_abi.EcoTrajRow)), C.byref(n_rows), C.byref(status), C.byref(status_node),
+        _abi.ptr(fin, C.c_double), C.byref(st)), "eco_mpc_run")
+    return rows[:n_rows.value], status.value, status_node.value, fin, field_out, st.as_dict()
+
+
+def mpc_step(vehicle: Vehicle, route: Route, spat: SpatSchedule, x: StateVector, s: int, *, gamma: float,
+             grids: GridSpec, penalty: PenaltyConfig, horizon: int, terminal: Optional[TerminalCostField] = None,
+             backend: str = "b200", workers: int = 8, teleport: bool = True, perturb_ties: bool = False):
+    """Solve the truncated horizon at node s and return the first action
+    (mpc.py:281-337).  Raises StartStateInfeasibleError when no action at x
+    has a feasible continuation."""
+    n = route.node_count
+    if not 0 <= s < n - 1:
+        raise ValueError(f"start node {s} out of range for {n} route nodes")
+    if perturb_ties:
+        raise ValueError("perturb_ties is not supported by the B200 kernels")
+    h = min(horizon, n - 1 - s)
+    rows, status, _, fin, _, st = run_closed_loop(
+        vehicle, route, spat, x, gamma=gamma, grids=grids, penalty=penalty, horizon=horizon, backend=backend,
+        teleport=teleport, field=terminal, use_terminal_field=terminal is not None, start_node=s, max_steps=1)
+    if status == _abi.RUN_MISMATCH:
+        raise RuntimeError(f"solver/plant transition mismatch at node {s}")
+    if status == _abi.RUN_INFEASIBLE or (len(rows) and rows[0]["fallback"]):
+        raise StartStateInfeasibleError(
+            f"no admissible action from node {s} at v={x.v:.2f} m/s, soc={x.soc:.3f}, t={x.t:.1f} s "
+            f"(teleport={'on' if teleport else 'off'})")
+    if status != _abi.RUN_OK or not len(rows):
+        raise RuntimeError(f"plant step failed at node {s}")
+    r = rows[0]
+    return (ActionVector(t_eng=float(r["t_eng"]), t_bsg=float(r["t_bsg"])),
+            MpcStepInfo(predicted_next=StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2])),
+                        cost_to_go=float(r["cost_to_go"]), wait=float(r["wait_s"]),
+                        solve_wall_s=st["device_ms"] / 1e3, horizon=h))
+
+
+class EcoDrivingMPC:
+    """Receding-horizon controller with fit / control (mpc.py:344-411)."""
+
+    name = "mpc"
+
+    def __init__(self, vehicle: Vehicle, *, gamma: float = 0.5, grids: Optional[GridSpec] = None,
+                 penalty: Optional[PenaltyConfig] = None, horizon: int = 20, backend: str = "b200",
+                 workers: int = 8, teleport: bool = True, use_terminal_field: bool = True,
+                 perturb_ties: bool = False):
+        precision_of(backend)
+        self.vehicle = vehicle
+        self.gamma = gamma
+        self.grids = grids if grids is not None else GridSpec()
+        self.penalty = penalty if penalty is not None else PenaltyConfig()
+        self.horizon = horizon
+        self.backend = backend
+        self.workers = workers
+        self.teleport = teleport
+        self.use_terminal_field = use_terminal_field
+        self.perturb_ties = perturb_ties
+
+    def fit(self, route: Route, spat: SpatSchedule) -> "EcoDrivingMPC":
+        if self.horizon < 1:
+            raise ValueError("horizon must be >= 1")
+        self.route_ = route
+        self.spat_ = spat
+        self.terminal_field_ = (build_terminal_cost(route, self.vehicle, gamma=self.gamma, grids=self.grids,
+                                                    penalty=self.penalty, spat=spat, backend=self.backend)
+                                if self.use_terminal_field else None)
+        return self
+
+    def control(self, x: StateVector, s: int) -> ControlDecision:
+        self._check_fitted()
+        action, info = mpc_step(self.vehicle, self.route_, self.spat_, x, s, gamma=self.gamma, grids=self.grids,
+                                penalty=self.penalty, horizon=self.horizon, terminal=self.terminal_field_,
+                                backend=self.backend, teleport=self.teleport, perturb_ties=self.perturb_ties)
+        return ControlDecision(action=action, predicted_next=info.predicted_next, cost_to_go=info.cost_to_go,
+                               solver_wall_s=info.solve_wall_s)
+
+    def _check_fitted(self):
+        if not hasattr(self, "route_"):
+            raise RuntimeError("controller is not fitted: call fit(route, spat) first")
+
+
+_STATUS_TEXT = {
+    _abi.RUN_INFEASIBLE: "infeasible: no admissible action and no legal braking move at node {node}",
+    _abi.RUN_PLANT: "infeasible: plant step rejected the applied action at node {node}",
+}
+
+
+def simulate_closed_loop(route: Route, spat: SpatSchedule, controller: EcoDrivingMPC,
+                         x_start: Optional[StateVector] = None, *, backend_tag: Optional[str] = None,
+                         ) -> ClosedLoopTrajectory:
+    """Drive the route under a fitted controller (mpc.py:513-596), entirely
+    on the device: one eco_mpc_run call for all N-1 nodes."""
+    if not isinstance(controller, EcoDrivingMPC):
+        raise TypeError("simulate_closed_loop drives an EcoDrivingMPC on the device")
+    controller._check_fitted()
+    if x_start is None:
+        x_start = StateVector(v=0.0, soc=0.5, t=0.0)
+    traj = ClosedLoopTrajectory(route_name=route.name, controller=controller.name,
+                                backend=backend_tag if backend_tag is not None else controller.backend,
+                                delta_d=route.delta_d, x_start=x_start)
+    if route.node_count == 1:
+        traj.final_state = x_start
+        return traj
+    rows, status, node, fin, _, st = run_closed_loop(
+        controller.vehicle, route, spat, x_start, gamma=controller.gamma, grids=controller.grids,
+        penalty=controller.penalty, horizon=controller.horizon, backend=controller.backend,
+        teleport=controller.teleport, field=controller.terminal_field_,
+        use_terminal_field=controller.use_terminal_field)
+    if status == _abi.RUN_MISMATCH:
+        raise RuntimeError(f"solver/plant transition mismatch at node {node}")
+    traj.steps = _rows_to_steps(rows)
+    per = st["dominant_ms"] / 1e3 / max(len(rows), 1)
+    traj.solver_wall_s = [per] * len(rows)
+    traj.final_state = StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2]))
+    if status != _abi.RUN_OK:
+        traj.status = _STATUS_TEXT[status].format(node=node)
+    traj.stats = st
+    return traj
