@@ -110,7 +110,11 @@ def fields():
     t0 = time.perf_counter()
     f_urban = build_terminal_cost(route_u, vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN)
     print(f"urban field {time.perf_counter() - t0:.1f}s", flush=True)
-    np.savez_compressed(HERE / "fields.npz", short_small=f_small.values, urban_default=f_urban.values)
+    nodes = np.array([0, 79, 80, 150, 349, 520, 610, 698, 699])
+    np.savez_compressed(HERE / "fields.npz", short_small=f_small.values, urban_nodes=nodes,
+                        urban_slices=f_urban.values[nodes])
+    (HERE / "fields_urban.json").write_text(json.dumps({"digest": table_digest(f_urban.values),
+                                                        "shape": list(f_urban.values.shape)}))
 
 
 def loop_short():

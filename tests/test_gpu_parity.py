@@ -1,0 +1,302 @@
+"""CUDA path vs the reference (golden fixtures) and the pinned CPU oracle.
+
+Bar (north_star / SURVEY §8c):
+  * backend "b200-fp64": bitwise equal — max |dJ| = 0, 0 policy mismatches,
+    closed-loop trajectories identical row for row;
+  * backend "b200" (f32 value path, f64 geometry): toys bitwise (dyadic
+    arithmetic is exact in f32); on the plant, finite-mask agreement >= 99.9 %,
+    both-finite |dJ| / max(1, |J|) <= 1e-4 at p99.9 and <= 1e-3 max, argmin
+    agreement >= 99.9 %; closed-loop fuel and travel time within 0.1 %.
+"""
+
+import math
+
+import numpy as np
+import pytest
+from conftest import golden_json, golden_npz
+
+from _toys import random_toy
+from oracle import oracle as O
+from paper_2104_01284_b200 import (EcoDrivingMPC, GridSpec, PenaltyConfig, StartStateInfeasibleError, StateVector,
+                                   backward_step, build_context, build_terminal_cost, mpc_step, simulate_closed_loop,
+                                   solve_horizon, solve_toy, table_digest)
+
+pytestmark = pytest.mark.gpu
+
+PEN = PenaltyConfig()
+SMALL = GridSpec(n_v=12, n_soc=8, n_t=40, n_t_eng=8, n_t_bsg=10, horizon_steps=8)
+TRAJ_FIELDS = ("s", "v", "soc", "t", "t_eng", "t_bsg", "brake_force", "gear", "wait_s", "dt_move_s",
+               "fuel_inc_g", "accel", "cost_to_go", "fallback")
+
+# f32 tolerance of the cost-to-go (stated in DESIGN.md §5)
+REL_P999 = 1e-4
+REL_MAX = 1e-3
+
+
+def fp32_agreement(J32, P32, J64, P64, j_inf=PEN.j_inf):
+    f32, f64 = J32 < j_inf, J64 < j_inf
+    mask_agree = float(np.mean(f32 == f64))
+    both = f32 & f64
+    rel = np.abs(J32[both] - J64[both]) / np.maximum(1.0, np.abs(J64[both]))
+    pol = float(np.mean(P32[both] == P64[both])) if both.any() else 1.0
+    return mask_agree, (float(np.quantile(rel, 0.999)) if rel.size else 0.0), \
+        (float(rel.max()) if rel.size else 0.0), pol
+
+
+# ------------------------------------------------------------------ toys
+
+@pytest.mark.parametrize("backend", ["b200-fp64", "b200"])
+@pytest.mark.parametrize("seed", range(25))
+def test_toys_equal_reference(seed, backend):
+    g = golden_npz("toys.npz")
+    toy = random_toy(seed)
+    J, P = solve_toy(toy, backend=backend)
+    assert np.array_equal(J[0], g[f"enum_{seed}"])
+    for k in range(toy.horizon + 1):
+        assert np.array_equal(J[k], g[f"J_{seed}_{k}"])
+    for k in range(toy.horizon):
+        assert np.array_equal(P[k], g[f"P_{seed}_{k}"])
+
+
+def test_toy_all_infeasible():
+    toy = random_toy(13, horizon=1)
+    toy.stage1[0]["ok"][:] = 0
+    J, P = solve_toy(toy, backend="b200")
+    assert np.all(J[0] >= toy.j_inf) and np.all(P[0] == -1)
+
+
+def test_toy_tie_rule_lowest_flat_action():
+    toy = random_toy(11, horizon=1)
+    t = toy.stage1[0]
+    t["ok"][:] = 1
+    t["c1"][:] = 0.5
+    t["pbat"][:] = 0.0
+    t["dt"][:] = 2.0
+    t["v2"][:] = 1.0 if toy.v_axis.shape[0] > 1 else 0.0
+    toy.arr_green[0][:] = 1
+    toy.dep_ok[0][:] = 1
+    toy.wait[0][:] = 0.0
+    toy.src_kinds[0] = 0
+    toy.terminal[:] = 0.0
+    for backend in ("b200", "b200-fp64"):
+        _, P = solve_toy(toy, backend=backend)
+        feas = P[0] >= 0
+        assert feas.any() and np.all(P[0][feas] == 0)
+
+
+def test_toy_red_arrival_gate():
+    toy = random_toy(5, horizon=1)
+    t = toy.stage1[0]
+    t["ok"][:] = 1
+    t["c1"][:] = 1.0
+    t["pbat"][:] = 0.0
+    t["dt"][:] = 2.0
+    toy.src_kinds[0] = 0
+    toy.dep_ok[0][:] = 1
+    toy.wait[0][:] = 0.0
+    toy.terminal[:] = 0.0
+    toy.arr_green[0][:] = 0
+    t["v2"][:] = 1.0
+    J_moving, _ = solve_toy(toy, backend="b200")
+    t["v2"][:] = 0.0
+    J_stop, _ = solve_toy(toy, backend="b200")
+    assert np.all(J_moving[0] >= toy.j_inf)
+    assert (J_stop[0] < toy.j_inf).any()
+
+
+# ------------------------------------------------------------- plant solves
+
+@pytest.fixture(scope="module")
+def c1_ctx(vehicle, short_route):
+    route, spat = short_route
+    return build_context(vehicle, route, spat, 45, 50.0, grids=GridSpec(n_v=12, n_soc=8, n_t=40), penalty=PEN,
+                         gamma=0.5, horizon=20)
+
+
+def test_c1_fp64_bitwise(c1_ctx):
+    g = golden_npz("c1_short_s45_t50.npz")
+    res = solve_horizon(c1_ctx, backend="b200-fp64")
+    assert np.array_equal(np.stack([t.values for t in res.tables]), g["J"])
+    assert np.array_equal(np.stack([p.values for p in res.policies]), g["P"])
+
+
+def test_c1_fp32_within_tolerance(c1_ctx):
+    g = golden_npz("c1_short_s45_t50.npz")
+    res = solve_horizon(c1_ctx, backend="b200")
+    J = np.stack([t.values for t in res.tables])
+    P = np.stack([p.values for p in res.policies])
+    mask, p999, mx, pol = fp32_agreement(J[:-1], P, g["J"][:-1], g["P"])
+    assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (mask, p999, mx, pol)
+
+
+def test_c1_backward_step_matches(c1_ctx):
+    g = golden_npz("c1_short_s45_t50.npz")
+    J, P = backward_step(c1_ctx, 7, g["J"][8], backend="b200-fp64")
+    assert np.array_equal(J, g["J"][7]) and np.array_equal(P, g["P"][7])
+
+
+def test_c2_fp64_digests_and_live_count(vehicle, urban_route):
+    route, spat = urban_route
+    for i, case in enumerate(golden_json("c2_urban_digests.json")):
+        ctx = build_context(vehicle, route, spat, case["s"], case["t_start"], grids=GridSpec(), penalty=PEN,
+                            gamma=0.5, horizon=20)
+        res = solve_horizon(ctx, backend="b200-fp64", count_live=(i == 0))
+        assert [table_digest(t.values) for t in res.tables] == case["J"]
+        assert [table_digest(p.values) for p in res.policies] == case["P"]
+        if i == 0:
+            assert (case["s"], case["t_start"]) == (60, 30.0)
+            assert res.stats["live_updates"] == 114_537_119
+
+
+def test_c2_fp32_tolerance(vehicle, urban_route):
+    route, spat = urban_route
+    for case in golden_json("c2_urban_digests.json"):
+        ctx = build_context(vehicle, route, spat, case["s"], case["t_start"], grids=GridSpec(), penalty=PEN,
+                            gamma=0.5, horizon=20)
+        r64 = solve_horizon(ctx, backend="b200-fp64")
+        r32 = solve_horizon(ctx, backend="b200")
+        J64 = np.stack([t.values for t in r64.tables[:-1]])
+        J32 = np.stack([t.values for t in r32.tables[:-1]])
+        P64 = np.stack([p.values for p in r64.policies])
+        P32 = np.stack([p.values for p in r32.policies])
+        mask, p999, mx, pol = fp32_agreement(J32, P32, J64, P64)
+        assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (case["s"], mask, p999, mx, pol)
+
+
+def test_c4_scenarios_fp64(vehicle):
+    from paper_2104_01284_b200.fixtures import make_route_urban
+    from paper_2104_01284_b200.route import load_route
+    for case in golden_json("c4_batch_digests.json"):
+        route, spat = load_route(make_route_urban(seed=case["seed"]))
+        ctx = build_context(vehicle, route, spat, case["s"], case["t_start"], grids=GridSpec(), penalty=PEN,
+                            gamma=0.5, horizon=20)
+        res = solve_horizon(ctx, backend="b200-fp64")
+        assert table_digest(res.tables[0].values) == case["J0"]
+        assert table_digest(res.policies[0].values) == case["P0"]
+
+
+def test_start_state_infeasible_raises(vehicle, short_route):
+    route, spat = short_route
+    ctx = build_context(vehicle, route, spat, 45, 50.0, grids=GridSpec(n_v=12, n_soc=8, n_t=40), penalty=PEN,
+                        gamma=0.5, horizon=4)
+    with pytest.raises(StartStateInfeasibleError):
+        solve_horizon(ctx, StateVector(v=13.0, soc=0.31, t=200.0), backend="b200")
+
+
+def test_solver_random_contexts_vs_oracle(vehicle, short_route):
+    """Seeded start nodes / clocks incl. the signal and red waits (standstill relocation)."""
+    route, spat = short_route
+    rng = np.random.default_rng(7)
+    grids = GridSpec(n_v=9, n_soc=7, n_t=24, n_t_eng=11, n_t_bsg=13)
+    for _ in range(6):
+        s = int(rng.integers(40, 70))
+        t = float(rng.uniform(-30.0, 150.0))
+        ctx = build_context(vehicle, route, spat, s, t, grids=grids, penalty=PEN, gamma=float(rng.uniform(0, 1)),
+                            horizon=int(rng.integers(1, 9)), teleport=bool(rng.integers(0, 2)))
+        J, P = O.solve_context(ctx)
+        res = solve_horizon(ctx, backend="b200-fp64")
+        for k in range(ctx.horizon):
+            assert np.array_equal(res.tables[k].values, J[k]), (s, t, k)
+            assert np.array_equal(res.policies[k].values, P[k]), (s, t, k)
+
+
+# ---------------------------------------------------------- field and loop
+
+def test_field_short_small_fp64(vehicle, short_route):
+    route, spat = short_route
+    f = build_terminal_cost(route, vehicle, gamma=0.5, grids=SMALL, penalty=PEN, backend="b200-fp64")
+    assert np.array_equal(f.values, golden_npz("fields.npz")["short_small"])
+
+
+def test_field_urban_default_fp64(vehicle, urban_route):
+    route, spat = urban_route
+    f = build_terminal_cost(route, vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN, backend="b200-fp64")
+    assert table_digest(f.values) == golden_json("fields_urban.json")["digest"]
+
+
+def test_field_urban_fp32(vehicle, urban_route):
+    route, spat = urban_route
+    gz = golden_npz("fields.npz")
+    g = gz["urban_slices"]
+    f = build_terminal_cost(route, vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN,
+                            backend="b200").values[gz["urban_nodes"]]
+    fin = g < PEN.j_inf
+    assert np.mean((f < PEN.j_inf) == fin) >= 0.999
+    both = fin & (f < PEN.j_inf)
+    assert np.max(np.abs(f[both] - g[both]) / np.maximum(1, np.abs(g[both]))) <= REL_MAX
+
+
+def rows_matrix(traj) -> np.ndarray:
+    return np.array([[float(getattr(st, f)) for f in TRAJ_FIELDS] for st in traj.steps])
+
+
+def test_closed_loop_short_fp64_identical(vehicle, short_route):
+    route, spat = short_route
+    g = golden_npz("loop_short_small.npz")
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=SMALL, penalty=PEN, horizon=8, backend="b200-fp64").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    assert traj.status == "ok" and traj.n_steps == route.node_count - 1
+    assert np.array_equal(rows_matrix(traj), g["rows"], equal_nan=True)
+    fs = traj.final_state
+    assert np.array_equal([fs.v, fs.soc, fs.t], g["final"])
+
+
+def test_closed_loop_short_fp32_totals(vehicle, short_route):
+    route, spat = short_route
+    g = golden_npz("loop_short_small.npz")
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=SMALL, penalty=PEN, horizon=8, backend="b200").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    assert traj.status == "ok"
+    fuel_ref = g["rows"][:, TRAJ_FIELDS.index("fuel_inc_g")].sum()
+    assert abs(traj.fuel_g - fuel_ref) <= 1e-3 * fuel_ref
+    assert abs(traj.final_state.t - g["final"][2]) <= 1e-3 * g["final"][2]
+    for st in traj.steps:
+        sid = route.traffic_lights.get(st.s)
+        if sid is not None and st.v > 0.0:
+            assert spat.timing(sid).is_green(st.t)
+
+
+def test_mpc_step_matches_gridded_policy(vehicle, short_route):
+    """mpc.py:168-191 contract: on-grid state -> the solved policy's action."""
+    route, spat = short_route
+    fld = build_terminal_cost(route, vehicle, gamma=0.5, grids=SMALL, penalty=PEN, backend="b200-fp64")
+    iv, jx = 4, 3
+    x = StateVector(v=float(SMALL.v_axis(route, 0)[iv]), soc=float(SMALL.soc_axis(vehicle)[jx]), t=0.0)
+    action, info = mpc_step(vehicle, route, spat, x, 0, gamma=0.5, grids=SMALL, penalty=PEN, horizon=8,
+                            terminal=fld, backend="b200-fp64")
+    ctx = build_context(vehicle, route, spat, 0, 0.0, grids=SMALL, penalty=PEN, gamma=0.5, horizon=8,
+                        terminal_field=fld.node_slice(8))
+    res = solve_horizon(ctx, backend="b200-fp64")
+    assert (action.t_eng, action.t_bsg) == res.policies[0].action(iv, jx, 0)
+    assert info.horizon == 8 and info.wait == 0.0 and math.isfinite(info.cost_to_go)
+
+
+def test_mpc_step_errors(vehicle, short_route):
+    route, spat = short_route
+    with pytest.raises(ValueError):
+        mpc_step(vehicle, route, spat, StateVector(5.0, 0.5, 0.0), route.node_count - 1, gamma=0.5, grids=SMALL,
+                 penalty=PEN, horizon=8)
+    _, info = mpc_step(vehicle, route, spat, StateVector(8.0, 0.5, 0.0), route.node_count - 2, gamma=0.5,
+                       grids=SMALL, penalty=PEN, horizon=8)
+    assert info.horizon == 1
+
+
+@pytest.mark.slow
+def test_closed_loop_urban_c2_fp64_identical(vehicle, urban_route):
+    route, spat = urban_route
+    g = golden_npz("loop_urban_c2.npz")
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN, horizon=20,
+                        backend="b200-fp64").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    assert traj.status == "ok"
+    assert np.array_equal(rows_matrix(traj), g["rows"], equal_nan=True)
+
+
+def test_closed_loop_urban_c2_fp32_within_0p1pct(vehicle, urban_route):
+    route, spat = urban_route
+    ref = golden_json("loop_urban_c2.json")
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN, horizon=20, backend="b200").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    assert traj.status == "ok" and traj.n_steps == ref["n_steps"]
+    assert abs(traj.fuel_g - ref["fuel_g"]) <= 1e-3 * ref["fuel_g"], (traj.fuel_g, ref["fuel_g"])
+    assert abs(traj.travel_time_s - ref["travel_time_s"]) <= 1e-3 * ref["travel_time_s"]
