@@ -1,0 +1,345 @@
+#!/usr/bin/env python3
+"""Benchmark: receding-horizon eco-driving DP on B200 (BASELINE.json metric).
+
+Workload at N=1 (BASELINE.json configs[1]): closed-loop MPC over
+the synthetic 700-node urban route with SPaT (5 signals, 2 stop signs),
+default grid (35 x 26 x 40 states, 23 x 30 actions), H = 20, gamma = 0.5,
+x0 = (0, 0.5, 0), terminal field on.  One *step* = one full closed-loop run:
+EcoDrivingMPC.fit (route geometry + signal-free terminal field, 699 (v,soc)
+sweeps) followed by 699 receding-horizon solves (13,790 Bellman stages), the
+exact-state argmin and the plant step at every node.
+
+  value   dense Bellman updates/s over the step, device-timed (CUDA events on
+          the launch stream), route/vehicle already uploaded (session built);
+  e2e     the same metric through the public API (EcoDrivingMPC.fit +
+          simulate_closed_loop) with host inputs and host outputs, including
+          allocation, H2D and the D2H of the trajectory and terminal field.
+
+N > 1 GPUs: the closed loop is sequential along the route, so ranks run
+independent replicas ("replicas only"): value = sum of updates /
+max over ranks of the device time.
+
+`--impl reference`: the reference algorithm's CPU implementation (the pinned
+C restatement in oracle/, all host threads) on a bounded sample of the same
+workload: fit + the first M receding-horizon steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Bellman state×control updates/sec; ms per receding-horizon DP solve"
+UNIT = "updates/s"
+FLOPS_PER_LIVE = 23          # 7 lerps x 3 + add + min per gathered candidate
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def fp32_peak_tflops(sm_count: int, sm_mhz: float) -> float:
+    """CUDA-core FP32 peak: 128 FMA lanes/SM x 2 flops x SMs x clock."""
+    return 2.0 * 128 * sm_count * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() in ("active", "1", "yes"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+
+def c2_inputs():
+    from paper_2104_01284_b200 import GridSpec, PenaltyConfig, StateVector, load_fixture_route, make_vehicle
+    vehicle = make_vehicle()
+    route, spat = load_fixture_route("urban", seed=0)
+    return vehicle, route, spat, GridSpec(), PenaltyConfig(), StateVector(v=0.0, soc=0.5, t=0.0)
+
+
+def dense_updates(route, grids, horizon, stages_loop):
+    n_u = grids.n_t_eng * grids.n_t_bsg
+    field = (route.node_count - 1) * grids.n_v * grids.n_soc * n_u
+    loop = stages_loop * grids.n_v * grids.n_soc * grids.n_t * n_u
+    return field, loop
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2104_01284_b200 import EcoDrivingMPC, simulate_closed_loop
+    from paper_2104_01284_b200.mpc import MpcSession
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    backend = "b200-fp64" if args.precision == "fp64" else "b200"
+    vehicle, route, spat, grids, pen, x0 = c2_inputs()
+    kw = dict(gamma=0.5, grids=grids, penalty=pen, horizon=20, backend=backend)
+    sess = MpcSession(vehicle, route, spat, **kw)
+
+    def step():
+        _, fst = sess.fit(want_field=False)
+        rows, status, _, fin, rst = sess.run(x0)
+        assert status == 0 and len(rows) == route.node_count - 1, (status, len(rows))
+        return fst, rst, rows
+
+    for _ in range(args.warmup):
+        step()
+    # one counting pass (outside the timed region): U_live of the whole loop
+    _, lst = sess.fit(want_field=False)
+    live = sess.run(x0, count_live=True, time_sweeps=False)[4]["live_updates"]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sweep_ms, loop_ms, stages, fit_dense = 0.0, 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            fst, rst, rows = step()
+            sweep_ms += rst["dominant_ms"]
+            loop_ms += rst["device_ms"]
+            stages += rst["stages"]
+            fit_dense += fst["dense_updates"]
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    t_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    field_u, loop_u = dense_updates(route, grids, 20, stages // args.steps)
+    per_step = field_u + loop_u
+    value = per_step * args.steps * world / (t_max / 1e3)
+    fuel = float(rows["fuel_inc_g"].sum())
+    t_end = float(rows["t"][-1] + rows["wait_s"][-1] + rows["dt_move_s"][-1])
+
+    # ------------------------------------------------ e2e through the public API
+    def api_step():
+        mpc = EcoDrivingMPC(vehicle, **kw).fit(route, spat)
+        traj = simulate_closed_loop(route, spat, mpc, x0)
+        assert traj.completed
+        return mpc, traj
+
+    api_step()
+    barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(args.steps):
+        mpc, traj = api_step()
+    a1.record(stream)
+    barrier()
+    e2e_ms = a0.elapsed_time(a1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = mpc.session_.h2d_bytes + 3 * 8
+    d2h = traj.n_steps * 120 + 3 * 8 + mpc.terminal_field_.values.nbytes + 4 * 3
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    peaks = measured_peaks()
+    props = torch.cuda.get_device_properties(local_rank)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = fp32_peak_tflops(props.multi_processor_count, sm_max)
+    if args.precision == "fp64":
+        peak /= 2.0     # B200: FP64 at half the FP32 rate
+    sweep_avg_s = sweep_ms / args.steps / 1e3
+    achieved = FLOPS_PER_LIVE * live / sweep_avg_s / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "stage_kernel_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(args.precision)
+    launches_per_step = rst["kernel_launches"] + fst["kernel_launches"]
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (reference fixture generators: urban route seed 0, synthetic 48V P0 vehicle)",
+        "config": {"workload": "C2: closed-loop MPC, urban 700-node route with SPaT, default grid 35x26x40 "
+                               "states x 23x30 controls, H=20, terminal field on (fit + 699 solves per step)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "working set (route geometry ~2.6 GB) exceeds L2; no flush between steps",
+                   "precision": args.precision},
+        "ms_per_solve": loop_ms / args.steps / (route.node_count - 1),
+        "sweep_ms_per_stage": sweep_ms / max(stages, 1),
+        "dense_updates_per_step": per_step,
+        "live_updates_per_step": live,
+        "closed_loop": {"fuel_g": fuel, "travel_time_s": t_end - x0.t, "steps": int(len(rows))},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "e2e": {"value": per_step * args.steps * world / (e2e_ms / 1e3), "unit": UNIT,
+                "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "roofline": {"bound": "fp32", "kernel": "bellman_stage_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"CUDA-core FP32 = 2 x 128 x {props.multi_processor_count} SMs x "
+                                    f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)"
+                                    + (" / 2 for FP64" if args.precision == "fp64" else ""),
+                     "algorithmic": f"{FLOPS_PER_LIVE} flop x {live} live gathers per step / summed sweep time"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+# ------------------------------------------------------------ CPU reference
+
+def cpu_sample(max_steps: int):
+    """Oracle (pinned C restatement of the reference, all host threads) on the
+    C2 workload: terminal field + the first max_steps receding-horizon steps."""
+    from oracle import oracle as O
+    vehicle, route, spat, grids, pen, x0 = c2_inputs()
+    threads = O.threads_available()
+    t0 = time.perf_counter()
+    fld = O.field_build(vehicle, route, spat, grids, pen, 0.5)
+    t1 = time.perf_counter()
+    r = O.mpc_run(vehicle, route, spat, grids, pen, 0.5, 20, (x0.v, x0.soc, x0.t), fld, parallel=True,
+                  threads=threads, max_steps=max_steps)
+    t2 = time.perf_counter()
+    stages = int(r["rows"]["horizon"].sum())
+    field_u, loop_u = dense_updates(route, grids, 20, stages)
+    return dict(updates=field_u + loop_u, seconds=t2 - t0, fit_s=t1 - t0, loop_s=t2 - t1,
+                steps=len(r["rows"]), threads=threads)
+
+
+def cpu_baseline(budget_s: float) -> dict:
+    probe = cpu_sample(5)
+    per_step = max(probe["loop_s"] / 5, 1e-3)
+    m = int(min(699, max(5, (budget_s - probe["fit_s"]) / per_step)))
+    s = cpu_sample(m)
+    return {"value": s["updates"] / s["seconds"], "unit": UNIT, "cores": s["threads"], "kind": "port",
+            "sample": f"C2 urban: terminal field ({699} (v,soc) sweeps) + first {s['steps']} MPC steps, "
+                      f"oracle/eco_oracle.c two-stage sweep, {s['threads']} OpenMP threads",
+            "seconds": s["seconds"], "ms_per_solve": s["loop_s"] * 1e3 / s["steps"]}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    budget = args.cpu_seconds
+    probe = cpu_sample(3)
+    per_step = max(probe["loop_s"] / 3, 1e-3)
+    m = int(min(699, max(3, (budget - probe["fit_s"]) / per_step)))
+    for _ in range(args.warmup):
+        cpu_sample(min(m, 3))
+    times, ups, last = [], [], None
+    for _ in range(args.steps):
+        last = cpu_sample(m)
+        times.append(last["seconds"])
+        ups.append(last["updates"])
+    value = sum(ups) / sum(times)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "C2: closed-loop MPC, urban route, default grid, H=20 (bounded sample)"},
+        "ms_per_solve": 1e3 * last["loop_s"] / last["steps"],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["threads"], "kind": "port",
+                         "sample": f"terminal field + first {last['steps']} MPC steps per step "
+                                   f"(oracle/eco_oracle.c, the pinned restatement of the reference kernels)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_rank()
+    if world != args.gpus and world == 1:
+        world = 1
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local_rank)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

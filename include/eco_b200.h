@@ -223,6 +223,28 @@ int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route,
                     EcoTrajRow* rows, int32_t* n_rows, int32_t* status,
                     int32_t* status_node, double* final_state, EcoStats* stats);
 
+/* Sessions: a route-resident solver for serving many closed loops.
+ * create  — upload plant / route, allocate all device buffers (no compute);
+ * fit     — route-level transition geometry + terminal field
+ *           (EcoDrivingMPC.fit, mpc.py:379-391); field_in != NULL uploads a
+ *           precomputed field instead of building it; field_out optional;
+ * run     — closed loop from start_node for max_steps nodes (< 0: to the end)
+ *           (simulate_closed_loop, mpc.py:513-596); flags: ECO_RUN_COUNT_LIVE
+ *           counts gathers (slower), ECO_RUN_TIME_SWEEPS times the Bellman
+ *           sweeps with CUDA events (stats->dominant_ms). */
+typedef struct EcoSession EcoSession;
+#define ECO_RUN_COUNT_LIVE 1
+#define ECO_RUN_TIME_SWEEPS 2
+int32_t eco_session_create(const EcoPlant* plant, const EcoRoute* route,
+                           const EcoMpcConfig* cfg, EcoSession** out);
+int32_t eco_session_fit(EcoSession* sess, const double* field_in,
+                        double* field_out, EcoStats* stats);
+int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,
+                        const double* x_start, EcoTrajRow* rows, int32_t* n_rows,
+                        int32_t* status, int32_t* status_node,
+                        double* final_state, int32_t flags, EcoStats* stats);
+int32_t eco_session_destroy(EcoSession* sess);
+
 /* Batch of independent horizon solves sharing one route geometry (C4):
  * scenario i starts at node s[i], time t_start[i] with its own SPaT
  * (routes[i]).  Writes the start-node cost-to-go J0 (n_scen, n_v, n_soc, n_t)

@@ -25,6 +25,7 @@ MAX_WINDOWS = 8
 OK, ERR_ARG, ERR_CUDA, ERR_NODEV = 0, 1, 2, 3
 FP32, FP64 = 0, 1
 RUN_OK, RUN_INFEASIBLE, RUN_PLANT, RUN_MISMATCH = 0, 1, 2, 3
+RUN_COUNT_LIVE, RUN_TIME_SWEEPS = 1, 2
 
 _D = C.c_double
 _I = C.c_int32
@@ -203,6 +204,10 @@ def _declare(lib):
         "eco_field_build": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _PD, P(EcoStats)]),
         "eco_mpc_run": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _PD, _PD, _PD, P(EcoTrajRow), _PI,
                              _PI, _PI, _PD, P(EcoStats)]),
+        "eco_session_create": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), P(C.c_void_p)]),
+        "eco_session_fit": (_I, [C.c_void_p, _PD, _PD, P(EcoStats)]),
+        "eco_session_run": (_I, [C.c_void_p, _I, _I, _PD, P(EcoTrajRow), _PI, _PI, _PI, _PD, _I, P(EcoStats)]),
+        "eco_session_destroy": (_I, [C.c_void_p]),
         "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), _I, _PI, _PD, P(EcoMpcConfig), _PD, _PI,
                                  P(EcoStats)]),
     }

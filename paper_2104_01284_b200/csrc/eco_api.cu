@@ -7,9 +7,11 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "eco_kernels.cuh"
@@ -80,6 +82,35 @@ __global__ void to_external_kernel(const Real* __restrict__ src, double* __restr
     }
 }
 
+// (v, soc, t) levels are stored twice: copy 0 as-is and copy 1 shifted by one
+// element, so the stage kernel reads any two consecutive time samples with one
+// aligned 64-bit load.  level_stride() is the distance between levels.
+__host__ __device__ inline size_t level_copy(size_t ns) { return (ns + 15) & ~size_t(7); }
+__host__ __device__ inline size_t level_stride(size_t ns) { return 2 * level_copy(ns); }
+
+template <typename Real>
+__global__ void to_internal2_kernel(const double* __restrict__ src, Real* __restrict__ dst, size_t n, double j_inf) {
+    Real* d1 = dst + level_copy(n);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n + 8; i += (size_t)gridDim.x * blockDim.x) {
+        const Real x = i < n ? ((src[i] >= j_inf) ? (Real)INFINITY : (Real)src[i]) : (Real)INFINITY;
+        if (i < n) dst[i] = x; else dst[i] = (Real)INFINITY;
+        if (i > 0) d1[i - 1] = x;
+        if (i == n + 7) d1[i] = (Real)INFINITY;
+    }
+}
+
+// copy 0 of `levels` stacked levels -> contiguous f64 (infeasible -> j_inf)
+template <typename Real>
+__global__ void to_external_levels_kernel(const Real* __restrict__ src, double* __restrict__ dst, size_t n,
+                                          int levels, double j_inf) {
+    const size_t total = n * levels;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t l = i / n, e = i - l * n;
+        const double x = (double)src[l * level_stride(n) + e];
+        dst[i] = (x < j_inf) ? x : j_inf;
+    }
+}
+
 inline unsigned grid_for(size_t n, unsigned block = 256) {
     size_t g = (n + block - 1) / block;
     if (g > 148u * 32u) g = 148u * 32u;
@@ -107,81 +138,165 @@ struct EventTimer {
     }
 };
 
+inline int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
 // --------------------------------------------------------- geometry store
 template <typename Real>
 struct Geometry {
     GeomDims dims{};
-    DBuf<uint32_t> meta;
-    DBuf<int32_t> zoff;
-    DBuf<Real> c1, wv, wz, wx;
+    DBuf<int32_t> count, u, gmax;
+    DBuf<int64_t> row_off;
     DBuf<double> dt, c1d, pbat;
-    DBuf<int16_t> jxlo;
+    DBuf<ActRec<Real>> act;
+    DBuf<RowRec<Real>> row;
+    DBuf<RowRec2<Real>> row2;
+    DBuf<TilePlan> tiles;
+    int h_gmax[4] = {0, 0, 0, 0};     // max feasible actions of a plane
+    int64_t rows_total = 0;
+    int tj = 0, nchunk = 0, band_cap = 0;   // stage-kernel tile shape the plans were built for
 
-    void alloc(int P, int nv, int nx, int U) {
+    void alloc(int P, int nv, int U) {
         const size_t np = (size_t)P * nv * U;
-        meta.alloc(np); zoff.alloc(np); c1.alloc(np); wv.alloc(np); wz.alloc(np);
-        dt.alloc(np); c1d.alloc(np); pbat.alloc(np);
-        jxlo.alloc(np * nx); wx.alloc(np * nx);
+        count.alloc((size_t)P * nv); row_off.alloc((size_t)P * nv); gmax.alloc(4);
+        u.alloc(np); dt.alloc(np); c1d.alloc(np); pbat.alloc(np); act.alloc(np);
     }
     PairGeom<Real> view() {
-        return PairGeom<Real>{meta.p, zoff.p, c1.p, wv.p, wz.p, dt.p, c1d.p, pbat.p, jxlo.p, wx.p};
+        return PairGeom<Real>{count.p, row_off.p, u.p, dt.p, c1d.p, pbat.p, act.p, row.p, gmax.p};
     }
 };
 
-// Computes pair + SoC geometry for P plans (dims filled by the caller).
+// Compacted pair records + SoC row records for P plans (dims filled by the
+// caller).  The row buffer is sized from the feasible-pair count (kept across
+// rebuilds of the same route, so refits allocate nothing).
 template <typename Real>
 void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d_plans, const double* d_vaxes,
                     const double* d_te, const double* d_tb, const double* d_soc, const EcoStage1Tables& d_tab,
                     cudaStream_t st, int64_t* launches) {
     const GeomDims& g = G.dims;
-    G.alloc(g.P, g.nv, g.nx, g.U);
+    if (G.act.n != (size_t)g.P * g.nv * g.U) G.alloc(g.P, g.nv, g.U);
+    ECO_CUDA(cudaMemsetAsync(G.gmax.p, 0, 4 * sizeof(int32_t), st));
     dim3 grid(g.nv, g.P);
     geom_pairs_kernel<Real><<<grid, 256, 0, st>>>(d_plant, d_plans, d_vaxes, d_te, d_tb, g, G.view(), d_tab);
     ECO_CUDA(cudaGetLastError());
+    const int npi = g.P * g.nv;
+    geom_rowoff_kernel<<<1, 1024, 0, st>>>(G.count.p, G.row_off.p, npi, g.nx);
+    ECO_CUDA(cudaGetLastError());
+    int64_t last_off = 0;
+    int32_t last_cnt = 0;
+    ECO_CUDA(cudaMemcpyAsync(&last_off, G.row_off.p + npi - 1, sizeof last_off, cudaMemcpyDeviceToHost, st));
+    ECO_CUDA(cudaMemcpyAsync(&last_cnt, G.count.p + npi - 1, sizeof last_cnt, cudaMemcpyDeviceToHost, st));
+    ECO_CUDA(cudaMemcpyAsync(G.h_gmax, G.gmax.p, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ECO_CUDA(cudaStreamSynchronize(st));
+    G.rows_total = last_off + (int64_t)last_cnt * g.nx;
+    if (G.row.n < (size_t)std::max<int64_t>(1, G.rows_total)) G.row.alloc((size_t)std::max<int64_t>(1, G.rows_total));
     const size_t smem = (size_t)g.ntb * g.nx * (sizeof(double) + 1) + 16;
     if (smem > 48 * 1024)
         ECO_CUDA(cudaFuncSetAttribute(geom_soc_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     geom_soc_kernel<Real><<<grid, 256, smem, st>>>(d_plant, d_vaxes, d_tb, d_soc, g, G.view(),
                                                    d_tab.ok != nullptr ? 1 : 0);
     ECO_CUDA(cudaGetLastError());
-    if (launches) *launches += 2;
+    geom_unpack_u_kernel<<<npi, 256, 0, st>>>(G.u.p, G.count.p, g.U);
+    ECO_CUDA(cudaGetLastError());
+    // staging plans of the (v, soc, t) stage kernel's tiles
+    const int upr = (g.nt + kZP - 1) / kZP;
+    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", std::max(1, 32 / upr))));
+    G.nchunk = (g.nx + G.tj - 1) / G.tj;
+    G.band_cap = env_int("ECO_BAND_KB", 40) * 1024 / (int)sizeof(Real);
+    const size_t ntiles = (size_t)npi * G.nchunk;
+    if (G.tiles.n != ntiles) G.tiles.alloc(ntiles);
+    if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
+    dim3 tgrid(g.nv * G.nchunk, g.P);
+    geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
+        G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p);
+    ECO_CUDA(cudaGetLastError());
+    if (launches) *launches += 5;
 }
 
-constexpr int kTile = 128;
-constexpr int kSlices = 8;
+// Tile shape of the stage kernel: tj SoC rows x n_t, S threads per action
+// slice (multiple of 32 so every warp walks one action at a time).
+struct TileCfg {
+    int tj, nchunk, S, slices;
+    int count_max = 0, band_cap = 0;
+    size_t smem;
+};
+
 
 template <typename Real>
-StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int nt) {
+TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode) {
+    const int nx = G.dims.nx;
+    TileCfg t{};
+    if (mode == 1) {
+        t.tj = nx;                             // the whole (v, soc) plane per CTA
+        t.nchunk = 1;
+        t.S = (nx + 31) / 32 * 32;
+        if (t.S > 1024) throw ArgError{"n_soc too large for the field kernel"};
+        t.slices = std::max(1, std::min(env_int("ECO_FIELD_SLICES", 1024 / t.S), 1024 / t.S));
+        t.smem = align16((size_t)t.slices * t.S * sizeof(Real)) + (size_t)t.slices * t.S * sizeof(int32_t);
+    } else {
+        t.tj = G.tj;
+        t.nchunk = G.nchunk;
+        const int upr = (nt + kZP - 1) / kZP;
+        const int per_row = (nt % 2 == 0) ? upr : nt;       // fast path: kZP states / thread
+        t.S = (t.tj * per_row + 31) / 32 * 32;
+        if (t.S > 512) t.S = 512;
+        t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", std::max(1, 256 / t.S)), 512 / t.S));
+        t.count_max = std::max(1, G.h_gmax[0]);
+        t.band_cap = G.band_cap;
+        t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, t.band_cap).total;
+    }
+    if (t.smem > 227 * 1024) throw ArgError{"tile reduction buffers exceed shared memory"};
+    return t;
+}
+
+template <typename Real>
+StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int nt, const TileCfg& tc) {
     StageArgs<Real> a{};
     const GeomDims& g = G.dims;
     const size_t off = (size_t)p * g.nv * g.U;
-    a.meta = G.meta.p + off;
-    a.zoff = G.zoff.p + off;
-    a.c1 = G.c1.p + off;
-    a.wv = G.wv.p + off;
-    a.wz = G.wz.p + off;
+    a.count = G.count.p + (size_t)p * g.nv;
+    a.row_off = G.row_off.p + (size_t)p * g.nv;
+    a.u = G.u.p + off;
     a.dt = G.dt.p + off;
     a.c1d = G.c1d.p + off;
-    a.jxlo = G.jxlo.p + off * g.nx;
-    a.wx = G.wx.p + off * g.nx;
+    a.act = G.act.p + off;
+    a.row = G.row.p;
+    a.row2 = G.row2.p;
+    a.tiles = G.tiles.p + (size_t)p * g.nv * G.nchunk;
     a.v_src = d_vsrc;
     a.nv = g.nv;
     a.nx = g.nx;
     a.nt = nt;
     a.U = g.U;
+    a.tj = tc.tj;
+    a.nchunk = tc.nchunk;
+    a.S = tc.S;
+    a.slices = tc.slices;
+    a.count_max = tc.count_max;
+    a.band_cap = tc.band_cap;
     a.gamma = g.gamma;
     return a;
 }
 
+template <typename K>
+void set_smem_attr(K kernel, size_t smem) {
+    if (smem > 48 * 1024) ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
 template <typename Real, int MODE>
-void launch_stage(const StageArgs<Real>& a, bool count, cudaStream_t st) {
-    const int plane = a.nx * a.nt;
-    const int tiles = (plane + kTile - 1) / kTile;
-    const unsigned grid = (unsigned)(a.nv * tiles);
-    if (count)
-        bellman_stage_kernel<Real, MODE, kTile, kSlices, true><<<grid, kTile * kSlices, 0, st>>>(a);
-    else
-        bellman_stage_kernel<Real, MODE, kTile, kSlices, false><<<grid, kTile * kSlices, 0, st>>>(a);
+void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st) {
+    const unsigned grid = (unsigned)(a.nv * tc.nchunk);
+    const unsigned block = (unsigned)(tc.S * tc.slices);
+    if (MODE == 0) {
+        auto k = count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>;
+        set_smem_attr(k, tc.smem);
+        k<<<grid, block, tc.smem, st>>>(a);
+    } else {
+        set_smem_attr(field_stage_kernel<Real>, tc.smem);
+        field_stage_kernel<Real><<<grid, block, tc.smem, st>>>(a);
+    }
     ECO_CUDA(cudaGetLastError());
 }
 
@@ -274,17 +389,18 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     EventTimer all, sweep;
     all.start(st);
     Geometry<Real> G;
-    G.dims = GeomDims{H, nv, nx, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
+    G.dims = GeomDims{H, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
     // toy mode: each step has its own table; geometry built per plan below
     if (!tabs) build_geometry(G, d_plant.p, d_plans.p, d_v.p, d_te.p, d_tb.p, d_soc.p, tdev.view, st, &launches);
 
-    DBuf<Real> d_J((H + 1) * ns);
+    const size_t LV = level_stride(ns), LC = level_copy(ns);
+    DBuf<Real> d_J((H + 1) * LV);
     DBuf<int32_t> d_P((size_t)H * ns);
     DBuf<double> d_tmp(ns * (H + 1));
     DBuf<unsigned long long> d_live(1);
     ECO_CUDA(cudaMemsetAsync(d_live.p, 0, sizeof(unsigned long long), st));
     d_tmp.upload(terminal, ns, st);
-    to_internal_kernel<Real><<<grid_for(ns), 256, 0, st>>>(d_tmp.p, d_J.p + (size_t)H * ns, ns, pr->j_inf);
+    to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(d_tmp.p, d_J.p + (size_t)H * LV, ns, pr->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++launches;
     double sweep_ms = 0.0;
@@ -293,34 +409,39 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         for (int k = 0; k < H; ++k) {
             TablesDev tk;
             tk.upload(&tabs[k], (size_t)nv * U, st);
-            toyG[k].dims = GeomDims{1, nv, nx, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max,
+            toyG[k].dims = GeomDims{1, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max,
                                     pr->gamma, pr->dtg};
             build_geometry(toyG[k], d_plant.p, d_plans.p + k, d_v.p + (size_t)k * nv, d_te.p, d_tb.p, d_soc.p,
                            tk.view, st, &launches);
             ECO_CUDA(cudaStreamSynchronize(st));   // tk freed at scope end
         }
     }
+    std::vector<TileCfg> tcs(H);
+    for (int k = 0; k < H; ++k) tcs[k] = tile_cfg(tabs ? toyG[k] : G, nt, 0);
     sweep.start(st);
     for (int k = H - 1; k >= 0; --k) {
-        StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, d_v.p + (size_t)k * nv, nt)
-                                 : stage_args(G, k, d_v.p + (size_t)k * nv, nt);
+        const TileCfg& tc = tcs[k];
+        StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, d_v.p + (size_t)k * nv, nt, tc)
+                                 : stage_args(G, k, d_v.p + (size_t)k * nv, nt, tc);
         a.green = d_green.p + (size_t)k * nt;
         a.dep_ok = d_dep.p + (size_t)k * nt;
         a.t_dep = d_tdep.p + (size_t)k * nt;
         a.wait = d_wait.p + (size_t)k * nt;
-        a.J_next = d_J.p + (size_t)(k + 1) * ns;
-        a.J_out = d_J.p + (size_t)k * ns;
+        a.J_next = d_J.p + (size_t)(k + 1) * LV;
+        a.J_next1 = a.J_next + LC;
+        a.J_out = d_J.p + (size_t)k * LV;
+        a.J_out1 = a.J_out + LC;
         a.P_out = d_P.p + (size_t)k * ns;
         a.live = count ? d_live.p : nullptr;
         a.src_kind = plans[k].src_kind;
         a.t0 = pr->t0;
         a.dtg = pr->dtg;
         a.j_inf = (Real)pr->j_inf;
-        launch_stage<Real, 0>(a, count, st);
+        launch_stage<Real, 0>(a, tc, count, st);
         ++launches;
     }
     sweep.stop(st);
-    to_external_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns * (H + 1), pr->j_inf);
+    to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, H + 1, pr->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++launches;
     all.stop(st);
@@ -429,33 +550,33 @@ __global__ void field_init_kernel(const double* soc, const double* v_end, int nv
     }
 }
 
+// build_terminal_cost mpc.py:96-158 on the device: N-1 (v, soc) sweeps.
 template <typename Real>
-void field_build_impl(const EcoRoute* r, const EcoMpcConfig* c, Geometry<Real>& G, RouteDev& R,
-                      const double* d_soc, DBuf<double>& d_field_ext, cudaStream_t st, int64_t* launches,
-                      double* sweep_ms) {
-    const int n = r->node_count, nv = c->n_v, nx = c->n_soc;
+void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConfig* c, Geometry<Real>& G,
+                      RouteDev& R, const double* d_soc, DBuf<Real>& d_G, DBuf<double>& d_field_ext,
+                      cudaStream_t st, int64_t* launches, double* sweep_ms) {
+    const int nv = c->n_v, nx = c->n_soc;
     const size_t lvl = (size_t)nv * nx;
-    DBuf<Real> d_G((size_t)n * lvl);
-    d_field_ext.alloc((size_t)n * lvl);
     field_init_kernel<<<1, 256, 0, st>>>(d_soc, R.vaxes.p + (size_t)(n - 1) * nv, nv, nx, c->soc_target,
-                                         c->soc_weight, c->j_inf, r->kinds[n - 1] == ECO_NODE_STOP ? 1 : 0,
+                                         c->soc_weight, c->j_inf, kinds[n - 1] == ECO_NODE_STOP ? 1 : 0,
                                          d_field_ext.p + (size_t)(n - 1) * lvl);
     to_internal_kernel<Real><<<grid_for(lvl), 256, 0, st>>>(d_field_ext.p + (size_t)(n - 1) * lvl,
                                                             d_G.p + (size_t)(n - 1) * lvl, lvl, c->j_inf);
     ECO_CUDA(cudaGetLastError());
     *launches += 2;
+    const TileCfg tc = tile_cfg(G, 1, 1);
     EventTimer tm;
     tm.start(st);
     for (int s = n - 2; s >= 0; --s) {
-        StageArgs<Real> a = stage_args(G, s, R.vaxes.p + (size_t)s * nv, 1);
+        StageArgs<Real> a = stage_args(G, s, R.vaxes.p + (size_t)s * nv, 1, tc);
         a.J_next = d_G.p + (size_t)(s + 1) * lvl;
         a.J_out = d_G.p + (size_t)s * lvl;
         a.P_out = nullptr;
         // always-green field: a light is an ordinary launch point (mpc.py:141-142)
-        a.src_kind = r->kinds[s] == ECO_NODE_SIGNAL ? ECO_NODE_PLAIN : r->kinds[s];
-        a.dwell = r->stop_dwell;
+        a.src_kind = kinds[s] == ECO_NODE_SIGNAL ? ECO_NODE_PLAIN : kinds[s];
+        a.dwell = dwell;
         a.j_inf = (Real)c->j_inf;
-        launch_stage<Real, 1>(a, false, st);
+        launch_stage<Real, 1>(a, tc, false, st);
         ++*launches;
     }
     tm.stop(st);
@@ -495,7 +616,7 @@ struct RouteCtx {
     std::vector<double> h_soc;
     Geometry<Real> G;
 
-    void init(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, cudaStream_t st, int64_t* launches) {
+    void init(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, cudaStream_t st) {
         plant.alloc(1);
         plant.upload(p, 1, st);
         R.upload(r, c->n_v, st);
@@ -508,127 +629,206 @@ struct RouteCtx {
         h_soc = soc_axis(p, c->n_soc);
         soc.alloc(c->n_soc);
         soc.upload(h_soc.data(), c->n_soc, st);
-        G.dims = GeomDims{r->node_count - 1, c->n_v, c->n_soc, c->n_te * c->n_tb, c->n_te, c->n_tb,
+        G.dims = GeomDims{r->node_count - 1, c->n_v, c->n_soc, c->n_t, c->n_te * c->n_tb, c->n_te, c->n_tb,
                           r->delta_d, r->accel_min, r->accel_max, c->gamma, c->dt};
+        G.alloc(G.dims.P, G.dims.nv, G.dims.U);
+    }
+    // route-level geometry: stage-1 + SoC cells of every spatial step
+    void geometry(cudaStream_t st, int64_t* launches) {
         EcoStage1Tables none{};
         build_geometry(G, plant.p, plans.p, R.vaxes.p, te.p, tb.p, soc.p, none, st, launches);
     }
 };
 
-template <typename Real>
-void field_only_impl(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, double* field_out,
-                     EcoStats* stats) {
-    cudaStream_t st = 0;
-    int64_t launches = 0;
-    EventTimer all;
-    all.start(st);
-    RouteCtx<Real> ctx;
-    ctx.init(p, r, c, st, &launches);
-    DBuf<double> d_field;
-    double sweep_ms = 0.0;
-    field_build_impl<Real>(r, c, ctx.G, ctx.R, ctx.soc.p, d_field, st, &launches, &sweep_ms);
-    all.stop(st);
-    d_field.download(field_out, d_field.n, st);
-    ECO_CUDA(cudaStreamSynchronize(st));
-    if (stats) {
-        stats->device_ms = all.ms();
-        stats->dominant_ms = sweep_ms;
-        stats->dense_updates = (int64_t)(r->node_count - 1) * c->n_v * c->n_soc * c->n_te * c->n_tb;
-        stats->live_updates = -1;
-        stats->stages = r->node_count - 1;
-        stats->kernel_launches = launches;
-    }
-}
+// ------------------------------------------------------------- sessions
+// A session owns everything one route needs on the device: the uploaded
+// route / plant, the route-level geometry (one plan per spatial step), the
+// terminal field and the loop buffers.  create() only allocates and uploads;
+// fit() computes geometry + field (EcoDrivingMPC.fit, mpc.py:379-391);
+// run() drives the closed loop (simulate_closed_loop, mpc.py:513-596).
+struct SessionBase {
+    int precision = 0;
+    virtual ~SessionBase() = default;
+    virtual void fit(const double* field_in, double* field_out, EcoStats* stats) = 0;
+    virtual void run(int start_node, int max_steps, const double* x0, EcoTrajRow* rows, int32_t* n_rows,
+                     int32_t* status, int32_t* status_node, double* final_state, int flags, EcoStats* stats) = 0;
+};
+
+constexpr int kRunCountLive = 1;
+constexpr int kRunTimeSweeps = 2;
 
 template <typename Real>
-void mpc_run_impl(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, const double* x0,
-                  const double* field_in, double* field_out, EcoTrajRow* rows, int32_t* n_rows, int32_t* status,
-                  int32_t* status_node, double* final_state, EcoStats* stats) {
-    cudaStream_t st = 0;
-    int64_t launches = 0;
-    const int n = r->node_count, nv = c->n_v, nx = c->n_soc, nt = c->n_t, H = c->horizon;
-    const int U = c->n_te * c->n_tb;
-    const size_t ns = (size_t)nv * nx * nt;
-    EventTimer all, loop;
-    all.start(st);
+struct Session : SessionBase {
+    EcoMpcConfig cfg{};
+    std::vector<double> te_h, tb_h;
+    std::vector<int8_t> kinds;
+    int n = 0;
+    double stop_dwell = 0.0;
     RouteCtx<Real> ctx;
-    ctx.init(p, r, c, st, &launches);
-    DBuf<double> d_field;
-    double sweep_ms = 0.0;
-    if (c->use_terminal_field) {
-        if (field_in) {
-            d_field.alloc((size_t)n * nv * nx);
-            d_field.upload(field_in, d_field.n, st);
-        } else {
-            field_build_impl<Real>(r, c, ctx.G, ctx.R, ctx.soc.p, d_field, st, &launches, &sweep_ms);
+    DBuf<double> field;            // external f64 (n, nv, nx)
+    DBuf<Real> field_int;          // internal (n, nv, nx)
+    bool fitted = false;
+    DBuf<LoopState> state;
+    DBuf<uint8_t> green, dep;
+    DBuf<double> tdep, wait, tax;
+    DBuf<Real> J;
+    DBuf<int32_t> P;
+    DBuf<EcoTrajRow> rows;
+    DBuf<unsigned long long> live;
+    std::vector<cudaEvent_t> ev;
+    cudaStream_t st = 0;
+
+    Session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
+        cfg = *c;
+        te_h.assign(c->te_axis, c->te_axis + c->n_te);
+        tb_h.assign(c->tb_axis, c->tb_axis + c->n_tb);
+        cfg.te_axis = te_h.data();
+        cfg.tb_axis = tb_h.data();
+        n = r->node_count;
+        kinds.assign(r->kinds, r->kinds + n);
+        stop_dwell = r->stop_dwell;
+        ctx.init(p, r, &cfg, st);
+        const int nv = cfg.n_v, nx = cfg.n_soc, nt = cfg.n_t, H = cfg.horizon;
+        const size_t ns = (size_t)nv * nx * nt;
+        field.alloc((size_t)n * nv * nx);
+        field_int.alloc((size_t)n * nv * nx);
+        state.alloc(1);
+        green.alloc((size_t)(H + 1) * nt); dep.alloc((size_t)(H + 1) * nt);
+        tdep.alloc((size_t)(H + 1) * nt); wait.alloc((size_t)(H + 1) * nt); tax.alloc(nt);
+        J.alloc((size_t)(H + 1) * level_stride(ns));
+        P.alloc(ns);
+        rows.alloc(n - 1);
+        live.alloc(1);
+        ev.resize(2 * (size_t)n);
+        for (auto& e : ev) ECO_CUDA(cudaEventCreate(&e));
+        ECO_CUDA(cudaStreamSynchronize(st));
+    }
+    ~Session() override {
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+
+    void fit(const double* field_in, double* field_out, EcoStats* stats) override {
+        int64_t launches = 0;
+        EventTimer all;
+        all.start(st);
+        ctx.geometry(st, &launches);
+        double sweep_ms = 0.0;
+        const size_t lvl = (size_t)cfg.n_v * cfg.n_soc;
+        if (cfg.use_terminal_field) {
+            if (field_in) field.upload(field_in, (size_t)n * lvl, st);
+            else field_build_impl<Real>(kinds.data(), n, stop_dwell, &cfg, ctx.G, ctx.R, ctx.soc.p, field_int,
+                                        field, st, &launches, &sweep_ms);
+        }
+        all.stop(st);
+        if (field_out && cfg.use_terminal_field) field.download(field_out, (size_t)n * lvl, st);
+        ECO_CUDA(cudaStreamSynchronize(st));
+        fitted = true;
+        if (stats) {
+            stats->device_ms = all.ms();
+            stats->dominant_ms = sweep_ms;
+            stats->dense_updates = (cfg.use_terminal_field && !field_in)
+                                       ? (int64_t)(n - 1) * cfg.n_v * cfg.n_soc * cfg.n_te * cfg.n_tb : 0;
+            stats->live_updates = -1;
+            stats->stages = (cfg.use_terminal_field && !field_in) ? n - 1 : 0;
+            stats->kernel_launches = launches;
         }
     }
-    DBuf<LoopState> d_state(1);
-    LoopState h0{};
-    h0.x[0] = x0[0]; h0.x[1] = x0[1]; h0.x[2] = x0[2];
-    d_state.upload(&h0, 1, st);
-    DBuf<uint8_t> green((size_t)(H + 1) * nt), dep((size_t)(H + 1) * nt);
-    DBuf<double> tdep((size_t)(H + 1) * nt), wait((size_t)(H + 1) * nt), tax(nt);
-    Ladders lad{green.p, dep.p, tdep.p, wait.p, tax.p};
-    DBuf<Real> d_J((size_t)(H + 1) * ns);
-    DBuf<int32_t> d_P(ns);
-    DBuf<EcoTrajRow> d_rows(n - 1);
-    const int s_begin = c->start_node;
-    const int s_end = c->max_steps < 0 ? n - 1 : std::min(n - 1, s_begin + c->max_steps);
-    LoopCfg lc{nv, nx, nt, c->n_te, c->n_tb, U, H, c->teleport, c->use_terminal_field, c->dt, c->gamma,
-               c->soc_target, c->soc_weight, c->j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
-    int64_t stages = 0;
-    loop.start(st);
-    for (int s = s_begin; s < s_end; ++s) {
-        const int h = H < n - 1 - s ? H : n - 1 - s;
-        mpc_prepare_kernel<Real><<<1, 256, 0, st>>>(ctx.R.view, lc, d_state.p, s, h,
-                                                    c->use_terminal_field ? d_field.p : nullptr, lad,
-                                                    d_J.p + (size_t)h * ns);
-        ECO_CUDA(cudaGetLastError());
-        ++launches;
-        for (int k = h - 1; k >= 0; --k) {
-            StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt);
-            a.green = green.p + (size_t)(k + 1) * nt;
-            a.dep_ok = dep.p + (size_t)k * nt;
-            a.t_dep = tdep.p + (size_t)k * nt;
-            a.wait = wait.p + (size_t)k * nt;
-            a.J_next = d_J.p + (size_t)(k + 1) * ns;
-            a.J_out = d_J.p + (size_t)k * ns;
-            a.P_out = d_P.p;
-            a.status = &d_state.p->status;
-            a.src_kind = r->kinds[s + k];
-            a.t0_dev = tax.p;   // ladder origin depends on the device-resident clock
-            a.dtg = c->dt;
-            a.j_inf = (Real)c->j_inf;
-            launch_stage<Real, 0>(a, false, st);
+
+    void run(int start_node, int max_steps, const double* x0, EcoTrajRow* out_rows, int32_t* n_rows,
+             int32_t* status, int32_t* status_node, double* final_state, int flags, EcoStats* stats) override {
+        if (!fitted) throw ArgError{"session not fitted: call eco_session_fit first"};
+        if (start_node < 0 || start_node > n - 2) throw ArgError{"start_node out of range"};
+        const int nv = cfg.n_v, nx = cfg.n_soc, nt = cfg.n_t, H = cfg.horizon;
+        const int U = cfg.n_te * cfg.n_tb;
+        const size_t ns = (size_t)nv * nx * nt;
+        const bool count = flags & kRunCountLive;
+        const bool timed = flags & kRunTimeSweeps;
+        int64_t launches = 0;
+        LoopState h0{};
+        h0.x[0] = x0[0]; h0.x[1] = x0[1]; h0.x[2] = x0[2];
+        EventTimer all;
+        all.start(st);
+        state.upload(&h0, 1, st);
+        if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
+        Ladders lad{green.p, dep.p, tdep.p, wait.p, tax.p};
+        LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
+                   cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
+        const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
+        const TileCfg tc = tile_cfg(ctx.G, nt, 0);
+        int64_t stages = 0;
+        int nev = 0;
+        for (int s = start_node; s < s_end; ++s) {
+            const int h = H < n - 1 - s ? H : n - 1 - s;
+            const size_t LV = level_stride(ns), LC = level_copy(ns);
+            mpc_prepare_kernel<Real><<<1, 256, 0, st>>>(ctx.R.view, lc, state.p, s, h,
+                                                        cfg.use_terminal_field ? field.p : nullptr, lad,
+                                                        J.p + (size_t)h * LV, J.p + (size_t)h * LV + LC);
+            ECO_CUDA(cudaGetLastError());
             ++launches;
-            ++stages;
+            if (timed) ECO_CUDA(cudaEventRecord(ev[2 * nev], st));
+            for (int k = h - 1; k >= 0; --k) {
+                StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tc);
+                a.green = green.p + (size_t)(k + 1) * nt;
+                a.dep_ok = dep.p + (size_t)k * nt;
+                a.t_dep = tdep.p + (size_t)k * nt;
+                a.wait = wait.p + (size_t)k * nt;
+                a.J_next = J.p + (size_t)(k + 1) * LV;
+                a.J_next1 = a.J_next + LC;
+                a.J_out = J.p + (size_t)k * LV;
+                a.J_out1 = a.J_out + LC;
+                a.P_out = P.p;
+                a.status = &state.p->status;
+                a.live = count ? live.p : nullptr;
+                a.src_kind = kinds[s + k];
+                a.t0_dev = tax.p;   // ladder origin depends on the device-resident clock
+                a.dtg = cfg.dt;
+                a.j_inf = (Real)cfg.j_inf;
+                launch_stage<Real, 0>(a, tc, count, st);
+                ++launches;
+                ++stages;
+            }
+            if (timed) ECO_CUDA(cudaEventRecord(ev[2 * nev + 1], st));
+            ++nev;
+            mpc_decide_kernel<Real><<<1, kDecideThreads, 0, st>>>(ctx.plant.p, ctx.R.view, lc, state.p, s, h, lad,
+                                                                  J.p + LV, rows.p);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
         }
-        mpc_decide_kernel<Real><<<1, kDecideThreads, 0, st>>>(ctx.plant.p, ctx.R.view, lc, d_state.p, s, h, lad,
-                                                              d_J.p + ns, d_rows.p);
-        ECO_CUDA(cudaGetLastError());
-        ++launches;
+        all.stop(st);
+        LoopState hs{};
+        state.download(&hs, 1, st);
+        unsigned long long nlive = 0;
+        if (count) ECO_CUDA(cudaMemcpyAsync(&nlive, live.p, sizeof nlive, cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaStreamSynchronize(st));
+        rows.download(out_rows, hs.n_rows, st);
+        ECO_CUDA(cudaStreamSynchronize(st));
+        *n_rows = hs.n_rows;
+        *status = hs.status;
+        *status_node = hs.status_node;
+        final_state[0] = hs.x[0]; final_state[1] = hs.x[1]; final_state[2] = hs.x[2];
+        if (stats) {
+            double sweep_ms = 0.0;
+            for (int i = 0; timed && i < nev; ++i) {
+                float m = 0.f;
+                ECO_CUDA(cudaEventElapsedTime(&m, ev[2 * i], ev[2 * i + 1]));
+                sweep_ms += m;
+            }
+            stats->device_ms = all.ms();
+            stats->dominant_ms = timed ? sweep_ms : -1.0;
+            stats->dense_updates = stages * (int64_t)ns * U;
+            stats->live_updates = count ? (int64_t)nlive : -1;
+            stats->stages = stages;
+            stats->kernel_launches = launches;
+        }
     }
-    loop.stop(st);
-    all.stop(st);
-    LoopState hs{};
-    d_state.download(&hs, 1, st);
-    ECO_CUDA(cudaStreamSynchronize(st));
-    d_rows.download(rows, hs.n_rows, st);
-    if (field_out && c->use_terminal_field) d_field.download(field_out, (size_t)n * nv * nx, st);
-    ECO_CUDA(cudaStreamSynchronize(st));
-    *n_rows = hs.n_rows;
-    *status = hs.status;
-    *status_node = hs.status_node;
-    final_state[0] = hs.x[0]; final_state[1] = hs.x[1]; final_state[2] = hs.x[2];
-    if (stats) {
-        stats->device_ms = all.ms();
-        stats->dominant_ms = loop.ms();
-        stats->dense_updates = (int64_t)stages * (int64_t)ns * U;
-        stats->live_updates = -1;
-        stats->stages = stages;
-        stats->kernel_launches = launches;
-    }
+};
+
+SessionBase* make_session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
+    SessionBase* s;
+    if (c->precision == ECO_FP64) s = new Session<double>(p, r, c);
+    else s = new Session<float>(p, r, c);
+    s->precision = c->precision;
+    return s;
 }
 
 }  // namespace
@@ -692,14 +892,49 @@ int32_t eco_solve_tables(const EcoPlant* plant, const EcoProblem* prob, const Ec
     });
 }
 
+int32_t eco_session_create(const EcoPlant* plant, const EcoRoute* route, const EcoMpcConfig* cfg,
+                           EcoSession** out) {
+    return run_guarded([&] {
+        check_plant(plant);
+        check_cfg(cfg);
+        if (!route || !out) throw ArgError{"null pointer argument"};
+        *out = reinterpret_cast<EcoSession*>(make_session(plant, route, cfg));
+    });
+}
+
+int32_t eco_session_fit(EcoSession* sess, const double* field_in, double* field_out, EcoStats* stats) {
+    return run_guarded([&] {
+        if (!sess) throw ArgError{"null session"};
+        reinterpret_cast<SessionBase*>(sess)->fit(field_in, field_out, stats);
+    });
+}
+
+int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps, const double* x_start,
+                        EcoTrajRow* rows, int32_t* n_rows, int32_t* status, int32_t* status_node,
+                        double* final_state, int32_t flags, EcoStats* stats) {
+    return run_guarded([&] {
+        if (!sess || !x_start || !rows || !n_rows || !status || !status_node || !final_state)
+            throw ArgError{"null pointer argument"};
+        reinterpret_cast<SessionBase*>(sess)->run(start_node, max_steps, x_start, rows, n_rows, status, status_node,
+                                                  final_state, flags, stats);
+    });
+}
+
+int32_t eco_session_destroy(EcoSession* sess) {
+    delete reinterpret_cast<SessionBase*>(sess);
+    return ECO_OK;
+}
+
 int32_t eco_field_build(const EcoPlant* plant, const EcoRoute* route, const EcoMpcConfig* cfg, double* field_out,
                         EcoStats* stats) {
     return run_guarded([&] {
         check_plant(plant);
         check_cfg(cfg);
         if (!route || !field_out) throw ArgError{"null pointer argument"};
-        if (cfg->precision == ECO_FP64) field_only_impl<double>(plant, route, cfg, field_out, stats);
-        else field_only_impl<float>(plant, route, cfg, field_out, stats);
+        EcoMpcConfig c = *cfg;
+        c.use_terminal_field = 1;
+        std::unique_ptr<SessionBase> s(make_session(plant, route, &c));
+        s->fit(nullptr, field_out, stats);
     });
 }
 
@@ -712,12 +947,10 @@ int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route, const EcoMpcCo
         if (!route || !x_start || !rows || !n_rows || !status || !status_node || !final_state)
             throw ArgError{"null pointer argument"};
         if (cfg->start_node > route->node_count - 2) throw ArgError{"start_node out of range"};
-        if (cfg->precision == ECO_FP64)
-            mpc_run_impl<double>(plant, route, cfg, x_start, field_in, field_out, rows, n_rows, status, status_node,
-                                 final_state, stats);
-        else
-            mpc_run_impl<float>(plant, route, cfg, x_start, field_in, field_out, rows, n_rows, status, status_node,
-                                final_state, stats);
+        std::unique_ptr<SessionBase> s(make_session(plant, route, cfg));
+        s->fit(field_in, field_out, nullptr);
+        s->run(cfg->start_node, cfg->max_steps, x_start, rows, n_rows, status, status_node, final_state,
+               kRunTimeSweeps, stats);
     });
 }
 

@@ -1,13 +1,15 @@
-// eco_kernels.cuh — geometry and Bellman-sweep kernels.
+// eco_kernels.cuh — transition geometry and Bellman-sweep kernels.
 //
 // Design: the reference's per-step work splits into a part
-// that does not depend on the cost-to-go (the (v,u) transition physics of
-// dp_stage1_fill K:553-598, the per-(v,u,SoC) battery / SoC-cell lookup of
-// dp_stage2_sweep K:657-712) and the part that does (the V gather + argmin,
-// K:697-793 / K:536-545).  The first part depends only on the route node,
-// so it is computed ONCE per node for all stages (and shared by the terminal
-// field sweep and every receding-horizon solve of a closed loop); the per-
-// stage kernel is then a pure gather + min over memoized geometry.
+// that does not depend on the cost-to-go — the (v,u) transition physics of
+// dp_stage1_fill (K:553-598) and the per-(v,u,SoC) battery current / SoC cell
+// of dp_stage2_sweep (K:657-712) — and the part that does: the V gather and
+// the argmin (K:697-793 / K:536-545).  The first part depends only on the
+// route node, so it is computed ONCE per node (shared by the terminal field
+// sweep and every receding-horizon solve of a closed loop) and stored as
+// compact 16-byte records: one ActRec per feasible action of a source speed
+// plane (ascending flat index), one RowRec per (action, source SoC row).
+// The per-stage kernel is then a pure gather + min over those records.
 #pragma once
 
 #include "eco_plant.cuh"
@@ -21,93 +23,157 @@ struct DevPlan {
     double cos_g, sin_g, v0d, dvd;
 };
 
-// Pair record bits (per (plan, iv, u)); bit layout of PairGeom::meta.
-constexpr uint32_t kOk = 1u;       // transition_tail ok (K:374-392)
-constexpr uint32_t kGated = 2u;    // v_next > 0: arrival gated on green (K:496)
-constexpr uint32_t kDzh = 4u;      // wz > 0: time blend uses zlo+1 (K:513)
-constexpr uint32_t kDvh = 8u;      // wv > 0: speed blend uses ivlo+1
-constexpr int kIvShift = 8;
+// ActRec::meta bits: zoff (bits 0..15, clamped to n_t) | flags
+constexpr uint32_t kRecZoff = 0xFFFFu;
+constexpr uint32_t kRecDzh = 1u << 16;     // wz > 0: time blend uses zlo+1 (K:513)
+constexpr uint32_t kRecDvh = 1u << 17;     // ivhi = ivlo + 1
+constexpr uint32_t kRecGated = 1u << 18;   // v_next > 0: arrival gated on green (K:496)
 
 template <typename Real>
-struct PairGeom {                 // dense [P][n_v][U]
-    uint32_t* meta;
-    int32_t* zoff;
-    Real* c1;
-    Real* wv;
-    Real* wz;
+struct alignas(4 * sizeof(Real)) ActRec {  // per feasible action of a source plane
+    Real wv, wz, c1;                       // speed weight, time weight, stage cost (K:364-367)
+    uint32_t meta;
+};
+
+template <typename Real>
+struct alignas(16) RowRec {                // per (feasible action, source SoC row jx)
+    int32_t off;                           // (v,soc,t) index of (ivlo, jxlo, zoff); -1: SoC move off the hull
+    int32_t zlim;                          // ladder states z <= zlim land inside the ladder (K:514)
+    Real wx;                               // SoC weight
+    int32_t cell;                          // (v, soc) index ivlo * n_soc + jxlo (field sweep)
+};
+
+// Route-level geometry.  Pair arrays have a dense stride [P][nv][U] and are
+// compacted per (plan, iv) to the first count[p][iv] slots in ascending flat
+// action order; rows are fully compact at row_off[p][iv] + k * nx + jx.
+template <typename Real>
+struct PairGeom {
+    int32_t* count;               // [P][nv]
+    int64_t* row_off;             // [P][nv]
+    int32_t* u;                   // flat action index
     double* dt;                   // exact dt_move (standstill relocation)
-    double* c1d;                  // exact c1 (standstill hold cost in fp64 order)
+    double* c1d;                  // exact c1 (hold cost in f64 order)
     double* pbat;                 // exact battery power
-    int16_t* jxlo;                // [P][n_v][U][n_soc], -1 = infeasible SoC move
-    Real* wx;                     // [P][n_v][U][n_soc]
+    ActRec<Real>* act;            // [P][nv][U]
+    RowRec<Real>* row;            // compact
+    int32_t* gmax;                // [4]: max count over planes
 };
 
 struct GeomDims {
-    int P, nv, nx, U, nte, ntb;
+    int P, nv, nx, nt, U, nte, ntb;
     double delta_d, a_min, a_max, gamma, dtg;
 };
 
 // ------------------------------------------------------ stage-1 (v,u) pass
-// K:553-598 (+ transition_tail K:374-392).  grid (nv, P), block 256.
-// Table mode (tab_* != nullptr) reads the toy tables of dp_sweep_serial's
+// K:553-598 (+ transition_tail K:374-392), compacted.  grid (nv, P), block 256.
+// Table mode (tab.ok != nullptr) reads the toy tables of dp_sweep_serial's
 // use_tables path (K:476-493) instead of evaluating the plant.
 template <typename Real>
-__global__ void geom_pairs_kernel(const EcoPlant* __restrict__ plant, const DevPlan* __restrict__ plans,
-                                  const double* __restrict__ vaxes, const double* __restrict__ te_axis,
-                                  const double* __restrict__ tb_axis, GeomDims g, PairGeom<Real> out,
-                                  EcoStage1Tables tab) {
+__global__ void __launch_bounds__(256)
+geom_pairs_kernel(const EcoPlant* __restrict__ plant, const DevPlan* __restrict__ plans,
+                  const double* __restrict__ vaxes, const double* __restrict__ te_axis,
+                  const double* __restrict__ tb_axis, GeomDims g, PairGeom<Real> out, EcoStage1Tables tab) {
     const int iv = blockIdx.x, p = blockIdx.y;
     const EcoPlant& P = *plant;
     const DevPlan pl = plans[p];
     const double v = vaxes[(size_t)p * g.nv + iv];
     __shared__ StepPre q;
-    if (threadIdx.x == 0 && tab.ok == nullptr) q = step_pre(P, v, pl.cos_g, pl.sin_g);
+    __shared__ int s_warp[8];
+    __shared__ int s_base;
+    if (threadIdx.x == 0) {
+        if (tab.ok == nullptr) q = step_pre(P, v, pl.cos_g, pl.sin_g);
+        s_base = 0;
+    }
     __syncthreads();
     const size_t base = ((size_t)p * g.nv + iv) * g.U;
-    for (int u = threadIdx.x; u < g.U; u += blockDim.x) {
-        const int ite = u / g.ntb, itb = u - ite * g.ntb;
-        bool ok;
-        double v2, dt, pb, c1, wv, wz;
-        int ivlo, ivhi, zoff;
-        if (tab.ok == nullptr) {
-            StepOut o = step_eval_pre(P, v, te_axis[ite], tb_axis[itb], g.delta_d, g.a_min, g.a_max, 0.0, q);
-            ok = o.feas == kFeasOk;
-            if (ok && o.clamped && pl.dest_kind == ECO_NODE_PLAIN) ok = false;
-            if (ok && pl.dest_kind == ECO_NODE_STOP && o.v_next > 0.0) ok = false;
-            if (ok) ok = locate_uniform(o.v_next, pl.v0d, pl.dvd, g.nv, &ivlo, &ivhi, &wv);
-            v2 = o.v_next; dt = o.dt_move; pb = o.p_bat;
-            c1 = stage_cost(o.mf, dt, g.gamma);
-            if (ok) tcell_shift(dt, g.dtg, &zoff, &wz);
-        } else {
-            const size_t c = (size_t)iv * g.U + u;
-            ok = tab.ok[c] != 0;
-            v2 = tab.v2[c]; dt = tab.dt[c]; pb = tab.pbat[c]; c1 = tab.c1[c];
-            ivlo = tab.ivlo[c]; ivhi = tab.ivhi[c]; wv = tab.wv[c]; zoff = tab.zoff[c]; wz = tab.wz[c];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int r = 0; r < g.U; r += 256) {
+        const int u = r + threadIdx.x;
+        bool ok = false;
+        double v2 = 0, dt = 0, pb = 0, c1 = 0, wv = 0, wz = 0;
+        int ivlo = 0, ivhi = 0, zoff = 0;
+        if (u < g.U) {
+            const int ite = u / g.ntb, itb = u - ite * g.ntb;
+            if (tab.ok == nullptr) {
+                StepOut o = step_eval_pre(P, v, te_axis[ite], tb_axis[itb], g.delta_d, g.a_min, g.a_max, 0.0, q);
+                ok = o.feas == kFeasOk;
+                if (ok && o.clamped && pl.dest_kind == ECO_NODE_PLAIN) ok = false;
+                if (ok && pl.dest_kind == ECO_NODE_STOP && o.v_next > 0.0) ok = false;
+                if (ok) ok = locate_uniform(o.v_next, pl.v0d, pl.dvd, g.nv, &ivlo, &ivhi, &wv);
+                v2 = o.v_next; dt = o.dt_move; pb = o.p_bat;
+                c1 = stage_cost(o.mf, dt, g.gamma);
+                if (ok) tcell_shift(dt, g.dtg, &zoff, &wz);
+            } else {
+                const size_t c = (size_t)iv * g.U + u;
+                ok = tab.ok[c] != 0;
+                v2 = tab.v2[c]; dt = tab.dt[c]; pb = tab.pbat[c]; c1 = tab.c1[c];
+                ivlo = tab.ivlo[c]; ivhi = tab.ivhi[c]; wv = tab.wv[c]; zoff = tab.zoff[c]; wz = tab.wz[c];
+            }
         }
-        uint32_t m = 0;
+        // ordered block compaction: ballot + warp prefix + block prefix
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) s_warp[wid] = __popc(bal);
+        __syncthreads();
+        int wbase = 0, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            if (w < wid) wbase += s_warp[w];
+            total += s_warp[w];
+        }
         if (ok) {
-            m = kOk | (v2 > 0.0 ? kGated : 0u) | (wz > 0.0 ? kDzh : 0u) | (ivhi != ivlo ? kDvh : 0u) |
-                ((uint32_t)ivlo << kIvShift);
+            const size_t k = base + s_base + wbase + __popc(bal & ((1u << lane) - 1u));
+            // flat index; ivlo parked in the high half until the SoC pass has used it
+            out.u[k] = u | (ivlo << 16);
+            out.dt[k] = dt;
+            out.c1d[k] = c1;
+            out.pbat[k] = pb;
+            ActRec<Real> a;
+            a.wv = (Real)wv;
+            a.wz = (Real)wz;
+            a.c1 = (Real)c1;
+            // zoff saturates at n_t: any larger shift leaves the ladder
+            a.meta = (uint32_t)min(zoff, g.nt) | (wz > 0.0 ? kRecDzh : 0u) | (ivhi != ivlo ? kRecDvh : 0u) |
+                     (v2 > 0.0 ? kRecGated : 0u);
+            out.act[k] = a;
         }
-        out.meta[base + u] = m;
-        out.zoff[base + u] = ok ? zoff : 0;
-        out.c1[base + u] = (Real)(ok ? c1 : 0.0);
-        out.wv[base + u] = (Real)(ok ? wv : 0.0);
-        out.wz[base + u] = (Real)(ok ? wz : 0.0);
-        out.dt[base + u] = ok ? dt : 0.0;
-        out.c1d[base + u] = ok ? c1 : 0.0;
-        out.pbat[base + u] = ok ? pb : 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += total;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) {
+        out.count[(size_t)p * g.nv + iv] = s_base;
+        atomicMax(&out.gmax[0], s_base);
+    }
+}
+
+// exclusive scan of count * nx -> row_off (one block; P * nv entries)
+__global__ void geom_rowoff_kernel(const int32_t* __restrict__ count, int64_t* __restrict__ row_off, int n,
+                                   int nx) {
+    __shared__ int64_t s_part[1024];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    int64_t acc = 0;
+    for (int i = b; i < e; ++i) acc += (int64_t)count[i] * nx;
+    s_part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) { const int64_t x = s_part[t]; s_part[t] = run; run += x; }
+    }
+    __syncthreads();
+    acc = s_part[threadIdx.x];
+    for (int i = b; i < e; ++i) { row_off[i] = acc; acc += (int64_t)count[i] * nx; }
 }
 
 // ------------------------------------------------------- SoC-cell pass
 // Battery current per (v, T_bsg, SoC) shared by the torque column (K:657-672),
-// then xi' = xi - dt*I/C_nom and its cell (K:498-506 / K:709-712).
-// grid (nv, P), block 256; per_action_pbat = toy mode (K:676-683).
+// then xi' = xi - dt*I/C_nom and its cell (K:498-506 / K:709-712) for every
+// compacted pair -> RowRec.  grid (nv, P), block 256; per_action_pbat = toy
+// mode (K:676-683).
 template <typename Real>
-__global__ void geom_soc_kernel(const EcoPlant* __restrict__ plant, const double* __restrict__ vaxes,
-                                const double* __restrict__ tb_axis, const double* __restrict__ soc_axis,
-                                GeomDims g, PairGeom<Real> out, int per_action_pbat) {
+__global__ void __launch_bounds__(256)
+geom_soc_kernel(const EcoPlant* __restrict__ plant, const double* __restrict__ vaxes,
+                const double* __restrict__ tb_axis, const double* __restrict__ soc_axis, GeomDims g,
+                PairGeom<Real> out, int per_action_pbat) {
     extern __shared__ double sm[];
     double* cur = sm;                                   // [ntb][nx]
     uint8_t* cur_ok = (uint8_t*)(sm + g.ntb * g.nx);    // [ntb][nx]
@@ -127,31 +193,143 @@ __global__ void geom_soc_kernel(const EcoPlant* __restrict__ plant, const double
         }
     }
     __syncthreads();
-    const size_t base = ((size_t)p * g.nv + iv) * g.U;
-    for (int i = threadIdx.x; i < g.U * g.nx; i += blockDim.x) {
-        const int u = i / g.nx, jx = i - u * g.nx;
-        const size_t gi = (base + u) * g.nx + jx;
-        int16_t lo16 = -1;
-        Real wxr = (Real)0;
-        if (out.meta[base + u] & kOk) {
-            double c;
-            bool okb;
-            if (per_action_pbat) {
-                okb = battery_current(P, out.pbat[base + u], soc_axis[jx], &c);
-            } else {
-                const int itb = u % g.ntb;
-                okb = cur_ok[itb * g.nx + jx] != 0;
-                c = cur[itb * g.nx + jx];
-            }
-            if (okb) {
-                const double xi2 = soc_axis[jx] - out.dt[base + u] * c / P.c_nom;
-                int lo, hi;
-                double w;
-                if (locate_uniform(xi2, x0, dx, g.nx, &lo, &hi, &w)) { lo16 = (int16_t)lo; wxr = (Real)w; }
+    const size_t pi = (size_t)p * g.nv + iv;
+    const size_t base = pi * g.U;
+    const int n = out.count[pi];
+    RowRec<Real>* rows = out.row + out.row_off[pi];
+    for (int i = threadIdx.x; i < n * g.nx; i += blockDim.x) {
+        const int k = i / g.nx, jx = i - k * g.nx;
+        const int packed = out.u[base + k];
+        const int ivlo = packed >> 16;
+        const ActRec<Real> a = out.act[base + k];
+        const int zoff = (int)(a.meta & kRecZoff);
+        double c;
+        bool okb;
+        if (per_action_pbat) {
+            okb = battery_current(P, out.pbat[base + k], soc_axis[jx], &c);
+        } else {
+            const int itb = (packed & 0xFFFF) % g.ntb;
+            okb = cur_ok[itb * g.nx + jx] != 0;
+            c = cur[itb * g.nx + jx];
+        }
+        RowRec<Real> ro;
+        ro.off = -1;
+        ro.zlim = -1;
+        ro.wx = (Real)0;
+        ro.cell = 0;
+        if (okb) {
+            const double xi2 = soc_axis[jx] - out.dt[base + k] * c / P.c_nom;
+            int lo, hi;
+            double w;
+            if (locate_uniform(xi2, x0, dx, g.nx, &lo, &hi, &w)) {
+                ro.cell = ivlo * g.nx + lo;
+                ro.off = ro.cell * g.nt + zoff;
+                ro.zlim = g.nt - 1 - zoff - ((a.meta & kRecDzh) ? 1 : 0);
+                ro.wx = (Real)w;
             }
         }
-        out.jxlo[gi] = lo16;
-        out.wx[gi] = wxr;
+        rows[k * g.nx + jx] = ro;
+    }
+}
+
+// strip the parked ivlo from the flat action indices (after the SoC pass)
+__global__ void geom_unpack_u_kernel(int32_t* __restrict__ u, const int32_t* __restrict__ count, int U) {
+    const int pi = blockIdx.x;
+    const int n = count[pi];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) u[(size_t)pi * U + k] &= 0xFFFF;
+}
+
+template <typename Real>
+struct alignas(16) RowRec2 {   // shared-memory row record: band bases of the two speed corners
+    int32_t blo, bhi;          // band index of (ivlo, jxlo, zoff) and (ivhi, jxlo, zoff)
+    int32_t zlim;
+    Real wx;
+};
+
+// Per-tile staging plan (per plan, source plane iv, SoC-row chunk): the
+// destination-plane row segments of the next-stage table the tile's actions
+// touch.  Built once per route; the stage kernel just copies the segments
+// into shared memory.  nseg < 0: footprint exceeds the cap (L1 path).
+constexpr int kMaxSeg = 40;
+struct TilePlan {
+    int32_t nseg;
+    int32_t band;                     // staged elements
+    int32_t gofs[kMaxSeg];            // element offset of (plane, first row, t = 0) within a level
+    int32_t len[kMaxSeg];             // elements (rows * n_t)
+    int32_t sofs[kMaxSeg];            // shared-memory offset (running sum of len)
+};
+
+// grid (nv * nchunk, P), block 256, dyn smem nv * 2 ints.
+template <typename Real>
+__global__ void __launch_bounds__(256)
+geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap, TilePlan* __restrict__ tiles,
+                  RowRec2<Real>* __restrict__ row2) {
+    extern __shared__ int32_t s_lohi[];
+    int32_t* s_lo = s_lohi;
+    int32_t* s_hi = s_lohi + d.nv;
+    __shared__ int32_t s_base[kMaxSeg + 1];
+    __shared__ int32_t s_segof[1024];      // plane -> segment base (or -1); nv <= 1024
+    __shared__ int s_ok;
+    const int p = blockIdx.y;
+    const int iv = blockIdx.x / nchunk, c = blockIdx.x - iv * nchunk;
+    const int j0 = c * tj, tja = min(tj, d.nx - j0);
+    const size_t pi = (size_t)p * d.nv + iv;
+    const int n = g.count[pi];
+    const RowRec<Real>* rows = g.row + g.row_off[pi] + j0;
+    const ActRec<Real>* acts = g.act + pi * d.U;
+    for (int q = threadIdx.x; q < d.nv; q += blockDim.x) { s_lo[q] = d.nx; s_hi[q] = -1; }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * tja; i += blockDim.x) {
+        const int k = i / tja, r = i - k * tja;
+        const RowRec<Real> ro = rows[(size_t)k * d.nx + r];
+        if (ro.off < 0) continue;
+        const int dlo = ro.cell / d.nx, jl = ro.cell - dlo * d.nx;
+        const int jh = jl + (ro.wx > (Real)0 ? 1 : 0);
+        const int dhi = dlo + ((acts[k].meta & kRecDvh) ? 1 : 0);
+        atomicMin(&s_lo[dlo], jl); atomicMax(&s_hi[dlo], jh);
+        if (dhi != dlo) { atomicMin(&s_lo[dhi], jl); atomicMax(&s_hi[dhi], jh); }
+    }
+    __syncthreads();
+    TilePlan* tp = tiles + pi * nchunk + c;
+    if (threadIdx.x == 0) {
+        int ns = 0, run = 0, ok = d.nv <= 1024;
+        for (int q = 0; q < d.nv && ok; ++q) {
+            s_segof[q] = -1;
+            if (s_hi[q] < s_lo[q]) continue;
+            if (ns == kMaxSeg) { ok = 0; break; }
+            const int len = (s_hi[q] - s_lo[q] + 1) * d.nt;
+            s_segof[q] = run;
+            tp->gofs[ns] = (q * d.nx + s_lo[q]) * d.nt;
+            tp->len[ns] = len;
+            tp->sofs[ns] = run;
+            run += len;
+            ++ns;
+        }
+        if (run > band_cap) ok = 0;
+        tp->nseg = ok ? ns : -1;
+        tp->band = ok ? run : 0;
+        s_ok = ok;
+        (void)s_base;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    RowRec2<Real>* out = row2 + g.row_off[pi] + j0;
+    for (int i = threadIdx.x; i < n * tja; i += blockDim.x) {
+        const int k = i / tja, r = i - k * tja;
+        const RowRec<Real> ro = rows[(size_t)k * d.nx + r];
+        RowRec2<Real> q;
+        q.blo = 0; q.bhi = 0; q.zlim = -1; q.wx = (Real)0;
+        if (ro.off >= 0) {
+            const ActRec<Real> ac = acts[k];
+            const int zoff = (int)(ac.meta & kRecZoff);
+            const int dlo = ro.cell / d.nx, jl = ro.cell - dlo * d.nx;
+            const int dhi = dlo + ((ac.meta & kRecDvh) ? 1 : 0);
+            q.blo = s_segof[dlo] + (jl - s_lo[dlo]) * d.nt + zoff;
+            q.bhi = s_segof[dhi] + (jl - s_lo[dhi]) * d.nt + zoff;
+            q.zlim = ro.zlim;
+            q.wx = ro.wx;
+        }
+        out[(size_t)k * d.nx + r] = q;
     }
 }
 
@@ -162,16 +340,15 @@ __global__ void geom_soc_kernel(const EcoPlant* __restrict__ plant, const double
 // bilin2_abs / interp3_abs (K:325-361) without per-corner tests.
 template <typename Real>
 struct StageArgs {
-    // geometry of this stage's plan
-    const uint32_t* meta;
-    const int32_t* zoff;
-    const Real* c1;
-    const Real* wv;
-    const Real* wz;
+    const int32_t* count;         // [nv] of this stage's plan
+    const int64_t* row_off;       // [nv]
+    const int32_t* u;             // [nv][U]
     const double* dt;
     const double* c1d;
-    const int16_t* jxlo;
-    const Real* wx;
+    const ActRec<Real>* act;      // [nv][U]
+    const RowRec<Real>* row;      // compact (absolute)
+    const RowRec2<Real>* row2;    // staged-path row records (same indexing as row)
+    const TilePlan* tiles;        // [nv][nchunk] of this stage's plan
     const double* v_src;
     // ladders (n_t): destination green mask, source standstill arrays
     const uint8_t* green;
@@ -180,11 +357,15 @@ struct StageArgs {
     const double* wait;
     const Real* J_next;
     Real* J_out;
+    const Real* J_next1;          // MODE 0: J_next shifted by one element (J_next1[i] = J_next[i+1])
+    Real* J_out1;                 // MODE 0: shifted copy of J_out
     int32_t* P_out;               // nullptr in field mode
     unsigned long long* live;     // nullptr unless counting
     const int32_t* status;        // closed loop: skip when nonzero (nullable)
     const double* t0_dev;         // closed loop: ladder origin on the device (nullable)
     int nv, nx, nt, U;
+    int tj, nchunk, S, slices;    // tile: tj SoC rows; S threads per action slice
+    int count_max, band_cap;      // staging capacity: actions per plane, band elements
     int src_kind;
     double t0, dtg, gamma, dwell;
     Real j_inf;
@@ -195,97 +376,361 @@ struct StageArgs {
 __device__ __forceinline__ double lerp(double a, double b, double w) { return a + w * (b - a); }
 __device__ __forceinline__ float lerp(float a, float b, float w) { return __fmaf_rn(w, b - a, a); }
 
-// MODE 0: (v, soc, t) step (dp_sweep_serial K:421-546 / dp_stage2_sweep).
-// MODE 1: (v, soc) terminal-field step (field_sweep K:801-865): no time
-//         axis, stop-sign dwell charged at the time price.
-template <typename Real, int MODE, int TILE, int SLICES, bool COUNT>
-__global__ void __launch_bounds__(TILE * SLICES)
-bellman_stage_kernel(StageArgs<Real> a) {
-    __shared__ Real s_best[SLICES][TILE];
-    __shared__ int32_t s_arg[SLICES][TILE];
-    if (a.status && *a.status != 0) return;
-    const int plane = a.nx * a.nt;
-    const int tiles_per_plane = (plane + TILE - 1) / TILE;
-    const int iv = blockIdx.x / tiles_per_plane;
-    const int f = (blockIdx.x - iv * tiles_per_plane) * TILE + (threadIdx.x % TILE);
-    const int slice = threadIdx.x / TILE;
-    const bool active = f < plane;
-    const int jx = active ? f / a.nt : 0;
-    const int z = active ? f - jx * a.nt : 0;
-    const double v = a.v_src[iv];
-    const bool skip = (a.src_kind == ECO_NODE_STOP && v > 0.0);   // K:458-459
-    const bool standstill = v == 0.0;
-    const int nt = a.nt, nx = a.nx;
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-    Real best = a.j_inf;
-    int32_t bu = -1;
+template <typename Real> struct Vec2;
+template <> struct Vec2<float> { using T = float2; };
+template <> struct Vec2<double> { using T = double2; };
+
+constexpr int kZP = 5;   // ladder states per thread on the fast path (6 time corners = 3 aligned pairs)
+
+// Pair arithmetic for the fast path: packed f32x2 on sm_100 (FFMA2/FADD2), and
+// the unfused reference expression tree component-wise in f64.
+template <typename Real> struct Pair { Real x, y; };
+__device__ __forceinline__ Pair<float> p_lerp(Pair<float> a, Pair<float> b, float w) {
+    const float2 d = __fadd2_rn(make_float2(b.x, b.y), make_float2(-a.x, -a.y));
+    const float2 r = __ffma2_rn(make_float2(w, w), d, make_float2(a.x, a.y));
+    return {r.x, r.y};
+}
+__device__ __forceinline__ Pair<double> p_lerp(Pair<double> a, Pair<double> b, double w) {
+    return {lerp(a.x, b.x, w), lerp(a.y, b.y, w)};
+}
+__device__ __forceinline__ Pair<float> p_addc(Pair<float> a, float c) {
+    const float2 r = __fadd2_rn(make_float2(c, c), make_float2(a.x, a.y));
+    return {r.x, r.y};
+}
+__device__ __forceinline__ Pair<double> p_addc(Pair<double> a, double c) { return {c + a.x, c + a.y}; }
+// t-blend of two neighbouring pairs: (a.x..a.y, b.x) -> (lerp(a.x,a.y), lerp(a.y,b.x))
+__device__ __forceinline__ Pair<float> p_tblend(Pair<float> a, Pair<float> b, float w) {
+    return p_lerp(a, Pair<float>{a.y, b.x}, w);
+}
+__device__ __forceinline__ Pair<double> p_tblend(Pair<double> a, Pair<double> b, double w) {
+    return {lerp(a.x, a.y, w), lerp(a.y, b.x, w)};
+}
+
+// cp.async (LDGSTS): global -> shared without a register round trip
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+template <typename Real>
+struct TileSmem {
+    size_t green, red_best, red_arg, rr, act, band, total;
+    __host__ __device__ TileSmem(int nt, int tj, int slices, int count_max, int band_cap) {
+        size_t o = 0;
+        green = o;    o = align16(o + (size_t)nt);
+        red_best = o; o = align16(o + (size_t)slices * tj * nt * sizeof(Real));
+        red_arg = o;  o = align16(o + (size_t)slices * tj * nt * sizeof(int32_t));
+        rr = o;       o = align16(o + (size_t)count_max * tj * sizeof(RowRec2<Real>));
+        act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
+        band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
+        total = o;
+    }
+};
+
+// Bellman stage over (v, soc, t) (dp_sweep_serial K:421-546 / dp_stage2_sweep
+// K:601-794).  One CTA = (source plane iv, tj SoC rows x all n_t).  Threads =
+// slices x S; a thread visits the plane's feasible actions slice, slice +
+// slices, ... in ascending flat order (strict <: lowest index wins ties) and
+// the slices merge lexicographically.
+//
+// Moving planes (v > 0) run the fast path: a thread owns kZP consecutive
+// ladder states of one row, whose 4 time corners t'..t'+3 it shares; the two
+// copies of J_next (as-is / shifted by one) make every corner pair one aligned
+// 64-bit load.  Standstill planes (v == 0: red-wait / dwell relocation,
+// K:519-535) run a per-state loop.
+template <typename Real, bool COUNT>
+__global__ void __launch_bounds__(512)
+bellman_stage_kernel(StageArgs<Real> a) {
+    if (a.status && *a.status != 0) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    using V2 = typename Vec2<Real>::T;
+    const int iv = blockIdx.x / a.nchunk;
+    const int j0 = (blockIdx.x - iv * a.nchunk) * a.tj;
+    const int nt = a.nt, nx = a.nx;
+    const int tja = min(a.tj, nx - j0);
+    const int plane = nx * nt;
+    const int tstates = tja * nt;
+    const double v = a.v_src[iv];
+    const int count = (a.src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : a.count[iv];   // K:458-459
+    const size_t obase = (size_t)iv * plane + (size_t)j0 * nt;
+    if (count == 0) {
+        for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
+            a.J_out[obase + f] = (Real)INFINITY;
+            if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
+            a.P_out[obase + f] = -1;
+        }
+        return;
+    }
+    const TileSmem<Real> L(nt, a.tj, a.slices, a.count_max, a.band_cap);
+    uint8_t* s_green = smem + L.green;
+    Real* s_best = (Real*)(smem + L.red_best);
+    int32_t* s_arg = (int32_t*)(smem + L.red_arg);
+    int red = 0, held = 0;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+        const uint8_t g = a.green[i];
+        s_green[i] = g;
+        red |= (g == 0);
+        if (v == 0.0) held |= (a.dep_ok[i] == 0) | (a.wait[i] > 0.0);
+    }
+    // any red arrival sample at all?  (plain / stop destinations: never)
+    const bool any_red = __syncthreads_or(red) != 0;
+    // a standstill plane whose node never holds (no red wait, no stop dwell,
+    // departures always allowed) moves exactly like a moving one (K:528-533)
+    const bool any_hold = __syncthreads_or(held) != 0;
+
+    const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
+    const RowRec<Real>* rows = a.row + a.row_off[iv] + j0;     // + k * nx + r
+    const int S = a.S;
+    const int slice = threadIdx.x / S;
+    const int tid = threadIdx.x - slice * S;
+    const int tj_nt = a.tj * nt;
     unsigned long long nlive = 0;
 
-    if (active && !skip) {
-        const size_t pbase = (size_t)iv * a.U;
-        // stop-sign dwell of the field sweep (K:825) / per-z hold of the 3-D sweep
-        const double hold_field = (MODE == 1 && a.src_kind == ECO_NODE_STOP && standstill)
-                                      ? (1.0 - a.gamma) * a.dwell : 0.0;
-        uint8_t dep = 1;
-        double hold_z = 0.0, tdep_z = 0.0;
-        if (MODE == 0 && standstill) { dep = a.dep_ok[z]; hold_z = a.wait[z]; tdep_z = a.t_dep[z]; }
-        if (dep) {
-            for (int u = slice; u < a.U; u += SLICES) {
-                const uint32_t m = __ldg(a.meta + pbase + u);
-                if (!(m & kOk)) continue;
-                const size_t gi = (pbase + u) * nx + jx;
-                const int jxlo = __ldg(a.jxlo + gi);
-                if (jxlo < 0) continue;
-                const Real wx = __ldg(a.wx + gi);
-                const int jxhi = jxlo + (wx > (Real)0 ? 1 : 0);
-                const int ivlo = (int)(m >> kIvShift);
-                const int ivhi = ivlo + ((m & kDvh) ? 1 : 0);
-                const Real wv = __ldg(a.wv + pbase + u);
-                int zlo = 0, zhi = 0;
-                Real wz = (Real)0;
-                double hold = 0.0;
-                if (MODE == 0) {
-                    const int zoff = __ldg(a.zoff + pbase + u);
-                    if (standstill && hold_z > 0.0) {      // red wait / stop dwell relocation K:523-527
-                        const double t2 = tdep_z + __ldg(a.dt + pbase + u);
-                        double w;
-                        const double t0 = a.t0_dev ? a.t0_dev[0] : a.t0;
-                        if (!locate_uniform(t2, t0, a.dtg, nt, &zlo, &zhi, &w)) continue;
-                        wz = (Real)w;
-                        hold = hold_z;
-                    } else {                                // constant ladder shift K:508-515
-                        zlo = z + zoff;
-                        zhi = zlo + ((m & kDzh) ? 1 : 0);
-                        if (zhi > nt - 1) continue;
-                        wz = __ldg(a.wz + pbase + u);
-                    }
-                    if ((m & kGated) && a.green[zlo] == 0) continue;   // K:516 / K:534
-                } else {
-                    hold = hold_field;
+    const bool fast = v > 0.0 || !any_hold;
+    const int chunk = blockIdx.x - iv * a.nchunk;
+    const TilePlan* tp = a.tiles ? a.tiles + (size_t)iv * a.nchunk + chunk : nullptr;
+    const int nseg = tp ? tp->nseg : -1;
+    Real* s_band = (Real*)(smem + L.band);
+    RowRec2<Real>* s_rr = (RowRec2<Real>*)(smem + L.rr);
+    ActRec<Real>* s_act = (ActRec<Real>*)(smem + L.act);
+    if (fast && nseg >= 0 && count <= a.count_max) {
+        // ---- stage with cp.async: the tile's footprint of J_next (precomputed
+        //      segments), its row records and the plane's action records
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+        const bool v16 = ((nt * (int)sizeof(Real)) & 15) == 0;
+        for (int sg = warp; sg < nseg; sg += nwarps) {
+            const Real* src = a.J_next + tp->gofs[sg];
+            Real* dst = s_band + tp->sofs[sg];
+            const int len = tp->len[sg];
+            if (v16) {
+                constexpr int per = 16 / sizeof(Real);
+                for (int i = lane * per; i < len; i += 32 * per) cp_async16(dst + i, src + i);
+            } else {
+                for (int i = lane; i < len; i += 32) {
+                    if (sizeof(Real) == 4) cp_async4(dst + i, src + i);
+                    else dst[i] = src[i];
                 }
-                if (COUNT) ++nlive;
-                const Real* J = a.J_next;
-                const size_t r00 = ((size_t)ivlo * nx + jxlo) * nt, r10 = ((size_t)ivhi * nx + jxlo) * nt;
-                const size_t r01 = ((size_t)ivlo * nx + jxhi) * nt, r11 = ((size_t)ivhi * nx + jxhi) * nt;
-                // bilin2_abs nesting (K:335-337): v inside, then soc; then t (K:361)
-                const Real lo0 = lerp(__ldg(J + r00 + zlo), __ldg(J + r10 + zlo), wv);
-                const Real hi0 = lerp(__ldg(J + r01 + zlo), __ldg(J + r11 + zlo), wv);
-                Real jn = lerp(lo0, hi0, wx);
-                if (zhi != zlo) {
-                    const Real lo1 = lerp(__ldg(J + r00 + zhi), __ldg(J + r10 + zhi), wv);
-                    const Real hi1 = lerp(__ldg(J + r01 + zhi), __ldg(J + r11 + zhi), wv);
-                    jn = lerp(jn, lerp(lo1, hi1, wx), wz);
-                }
-                // F = c1 + (1-gamma)*hold + Jn, left to right (K:542 / K:862)
-                Real F;
-                if (hold > 0.0) {
-                    const double c = __ldg(a.c1d + pbase + u) + (MODE == 0 ? (1.0 - a.gamma) * hold : hold);
-                    F = (Real)c + jn;
-                } else {
-                    F = __ldg(a.c1 + pbase + u) + jn;
-                }
-                if (F < best) { best = F; bu = u; }
             }
+        }
+        const RowRec2<Real>* rr_src = a.row2 + a.row_off[iv] + j0;
+        constexpr int rr16 = sizeof(RowRec2<Real>) / 16, act16 = sizeof(ActRec<Real>) / 16;
+        for (int i = threadIdx.x; i < count * tja * rr16; i += blockDim.x) {
+            const int e = i / rr16, h = i - e * rr16;
+            const int k = e / tja, r = e - k * tja;
+            cp_async16(reinterpret_cast<char*>(s_rr + k * a.tj + r) + 16 * h,
+                       reinterpret_cast<const char*>(rr_src + (size_t)k * nx + r) + 16 * h);
+        }
+        for (int i = threadIdx.x; i < count * act16; i += blockDim.x)
+            cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
+        cp_async_wait_all();
+        __syncthreads();
+        // ---------------- staged fast path: corners from shared memory
+        using PR = Pair<Real>;
+        const int upr = (nt + kZP - 1) / kZP;
+        const bool unit_ok = tid < tja * upr;
+        const int r = unit_ok ? tid / upr : 0;
+        const int z0 = unit_ok ? (tid - r * upr) * kZP : 0;
+        Real best[kZP];
+        int bk[kZP];
+#pragma unroll
+        for (int i = 0; i < kZP; ++i) { best[i] = a.j_inf; bk[i] = -1; }
+        if (unit_ok) {
+            const int slices = a.slices;
+            const RowRec2<Real>* rows2 = s_rr + r;
+            const int tjs = a.tj;
+            for (int k = slice; k < count; k += slices) {
+                const RowRec2<Real> ro = rows2[k * tjs];
+                if (z0 > ro.zlim) continue;                      // also: SoC move off the hull
+                const ActRec<Real> rc = s_act[k];
+                const Real* plo = s_band + ro.blo + z0;          // (ivlo, jxlo, t' = z0 + zoff)
+                const Real* phi = s_band + ro.bhi + z0;          // (ivhi, jxlo, t')
+                const int dx = ro.wx > (Real)0 ? nt : 0;
+                PR col[3];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    const PR c00{plo[2 * m], plo[2 * m + 1]}, c10{phi[2 * m], phi[2 * m + 1]};
+                    const PR c01{plo[dx + 2 * m], plo[dx + 2 * m + 1]}, c11{phi[dx + 2 * m], phi[dx + 2 * m + 1]};
+                    const PR lo = p_lerp(c00, c10, rc.wv);       // v inside (K:335-337)
+                    const PR hi = p_lerp(c01, c11, rc.wv);
+                    col[m] = p_lerp(lo, hi, ro.wx);              // then soc
+                }
+                Real F[kZP];
+                if (rc.meta & kRecDzh) {                         // then t (K:361)
+                    const PR j01 = p_addc(p_tblend(col[0], col[1], rc.wz), rc.c1);
+                    const PR j23 = p_addc(p_tblend(col[1], col[2], rc.wz), rc.c1);
+                    F[0] = j01.x; F[1] = j01.y; F[2] = j23.x; F[3] = j23.y;
+                    F[4] = rc.c1 + lerp(col[2].x, col[2].y, rc.wz);
+                } else {
+                    const PR j01 = p_addc(col[0], rc.c1);
+                    const PR j23 = p_addc(col[1], rc.c1);
+                    F[0] = j01.x; F[1] = j01.y; F[2] = j23.x; F[3] = j23.y;
+                    F[4] = rc.c1 + col[2].x;
+                }
+                if (any_red && (rc.meta & kRecGated)) {
+                    const int tz0 = z0 + (int)(rc.meta & kRecZoff);
+#pragma unroll
+                    for (int i = 0; i < kZP; ++i) {
+                        const bool ok = z0 + i <= ro.zlim && s_green[tz0 + i] != 0;   // K:516
+                        if (COUNT) nlive += ok;
+                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kZP; ++i) {
+                        const bool ok = z0 + i <= ro.zlim;
+                        if (COUNT) nlive += ok;
+                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kZP; ++i) {
+            const int z = z0 + i;
+            if (unit_ok && z < nt) {
+                s_best[slice * tj_nt + r * nt + z] = best[i];
+                s_arg[slice * tj_nt + r * nt + z] = bk[i];
+            }
+        }
+    } else if (fast && (nt & 1) == 0) {
+        // ---------------- fast path: constant ladder shift (K:508-518, K:528-533)
+        using PR = Pair<Real>;
+        const int upr = (nt + kZP - 1) / kZP;
+        const bool unit_ok = tid < tja * upr;
+        const int r = unit_ok ? tid / upr : 0;
+        const int z0 = unit_ok ? (tid - r * upr) * kZP : 0;
+        Real best[kZP];
+        int bk[kZP];
+#pragma unroll
+        for (int i = 0; i < kZP; ++i) { best[i] = a.j_inf; bk[i] = -1; }
+        if (unit_ok) {
+            const Real* __restrict__ J0 = a.J_next;
+            const Real* __restrict__ J1 = a.J_next1;
+            const int slices = a.slices;
+            const Real* __restrict__ s_g = nullptr;
+            (void)s_g;
+            for (int k = slice; k < count; k += slices) {
+                const RowRec<Real> ro = rows[(size_t)k * nx + r];
+                if (z0 > ro.zlim) continue;                      // also: SoC move off the hull
+                const ActRec<Real> rc = acts[k];
+                const unsigned dv = (rc.meta & kRecDvh) ? (unsigned)plane : 0u;
+                const unsigned dx = ro.wx > (Real)0 ? (unsigned)nt : 0u;
+                const unsigned i0 = (unsigned)(ro.off + z0);     // (ivlo, jxlo, t' = z0 + zoff)
+                // all four corner rows share the parity of i0 (plane, nt even)
+                const Real* base = ((i0 & 1u) ? J1 : J0) + (i0 & ~1u);
+                PR c[4][3];                                      // [corner row][t pair]
+                const unsigned offs[4] = {0u, dv, dx, dv + dx};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const V2* pp = reinterpret_cast<const V2*>(base + offs[q]);
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        const V2 t = __ldg(pp + m);
+                        c[q][m] = PR{t.x, t.y};
+                    }
+                }
+                PR col[3];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    const PR lo = p_lerp(c[0][m], c[1][m], rc.wv);   // v inside (K:335-337)
+                    const PR hi = p_lerp(c[2][m], c[3][m], rc.wv);
+                    col[m] = p_lerp(lo, hi, ro.wx);                  // then soc
+                }
+                Real F[kZP];
+                if (rc.meta & kRecDzh) {                         // then t (K:361)
+                    const PR j01 = p_addc(p_tblend(col[0], col[1], rc.wz), rc.c1);
+                    const PR j23 = p_addc(p_tblend(col[1], col[2], rc.wz), rc.c1);
+                    F[0] = j01.x; F[1] = j01.y; F[2] = j23.x; F[3] = j23.y;
+                    F[4] = rc.c1 + lerp(col[2].x, col[2].y, rc.wz);
+                } else {
+                    const PR j01 = p_addc(col[0], rc.c1);
+                    const PR j23 = p_addc(col[1], rc.c1);
+                    F[0] = j01.x; F[1] = j01.y; F[2] = j23.x; F[3] = j23.y;
+                    F[4] = rc.c1 + col[2].x;
+                }
+                const bool all_in = z0 + kZP - 1 <= ro.zlim;
+                if (all_in && !(any_red && (rc.meta & kRecGated))) {
+                    if (COUNT) nlive += kZP;
+#pragma unroll
+                    for (int i = 0; i < kZP; ++i)
+                        if (F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                } else {
+                    const bool gate = any_red && (rc.meta & kRecGated);
+                    const int tz0 = z0 + (int)(rc.meta & kRecZoff);  // arrival sample of state z0
+#pragma unroll
+                    for (int i = 0; i < kZP; ++i) {
+                        bool ok = z0 + i <= ro.zlim;
+                        if (gate && ok) ok = s_green[tz0 + i] != 0;  // K:516
+                        if (COUNT) nlive += ok;
+                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kZP; ++i) {
+            const int z = z0 + i;
+            if (unit_ok && z < nt) {
+                s_best[slice * tj_nt + r * nt + z] = best[i];
+                s_arg[slice * tj_nt + r * nt + z] = bk[i];
+            }
+        }
+    } else {
+        // ---------------- per-state path (standstill plane, odd n_t)
+        const double t0 = a.t0_dev ? a.t0_dev[0] : a.t0;
+        for (int f = tid; f < tstates; f += S) {
+            const int r = f / nt, z = f - r * nt;
+            Real best = a.j_inf;
+            int bk = -1;
+            uint8_t dep = 1;
+            double hold = 0.0, tdep = 0.0;
+            if (v == 0.0) { dep = a.dep_ok[z]; hold = a.wait[z]; tdep = a.t_dep[z]; }
+            const bool reloc = hold > 0.0;
+            for (int k = slice; dep && k < count; k += a.slices) {
+                const RowRec<Real> ro = rows[(size_t)k * nx + r];
+                if (ro.off < 0) continue;                        // SoC move off the hull
+                const ActRec<Real> rc = acts[k];
+                const int zoff = (int)(rc.meta & kRecZoff);
+                int zlo, zhi;
+                Real wz;
+                if (reloc) {                                     // red wait / dwell relocation K:523-527
+                    const double t2 = tdep + a.dt[(size_t)iv * a.U + k];
+                    double w;
+                    if (!locate_uniform(t2, t0, a.dtg, nt, &zlo, &zhi, &w)) continue;
+                    wz = (Real)w;
+                } else {                                         // constant ladder shift K:508-515 / K:528-533
+                    if (z > ro.zlim) continue;
+                    zlo = z + zoff;
+                    zhi = zlo + ((rc.meta & kRecDzh) ? 1 : 0);
+                    wz = rc.wz;
+                }
+                if ((rc.meta & kRecGated) && s_green[zlo] == 0) continue;
+                if (COUNT) ++nlive;
+                const Real* b = a.J_next + (ro.off - zoff);     // (ivlo, jxlo, t' = 0)
+                const int dv = (rc.meta & kRecDvh) ? plane : 0;
+                const int dx = ro.wx > (Real)0 ? nt : 0;
+                const Real lo0 = lerp(__ldg(b + zlo), __ldg(b + dv + zlo), rc.wv);
+                const Real hi0 = lerp(__ldg(b + dx + zlo), __ldg(b + dv + dx + zlo), rc.wv);
+                Real jn = lerp(lo0, hi0, ro.wx);
+                if (zhi != zlo) {
+                    const Real lo1 = lerp(__ldg(b + zhi), __ldg(b + dv + zhi), rc.wv);
+                    const Real hi1 = lerp(__ldg(b + dx + zhi), __ldg(b + dv + dx + zhi), rc.wv);
+                    jn = lerp(jn, lerp(lo1, hi1, ro.wx), wz);
+                }
+                Real F;
+                if (reloc) F = (Real)(a.c1d[(size_t)iv * a.U + k] + (1.0 - a.gamma) * hold) + jn;   // K:542
+                else F = rc.c1 + jn;
+                if (F < best) { best = F; bk = k; }
+            }
+            s_best[slice * tj_nt + f] = best;
+            s_arg[slice * tj_nt + f] = bk;
         }
     }
     if (COUNT && a.live) {
@@ -293,19 +738,75 @@ bellman_stage_kernel(StageArgs<Real> a) {
         for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
         if ((threadIdx.x & 31) == 0 && w) atomicAdd(a.live, w);
     }
-    s_best[slice][threadIdx.x % TILE] = best;
-    s_arg[slice][threadIdx.x % TILE] = bu;
     __syncthreads();
-    if (slice == 0 && active) {
-        for (int s = 1; s < SLICES; ++s) {
-            const int32_t u2 = s_arg[s][threadIdx.x];
-            if (u2 < 0) continue;
-            const Real b2 = s_best[s][threadIdx.x];
-            if (bu < 0 || b2 < best || (b2 == best && u2 < bu)) { best = b2; bu = u2; }
+    // ---- merge slices: lexicographic (F, k); k ascends with the flat index
+    const int32_t* u = a.u + (size_t)iv * a.U;
+    for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
+        Real best = s_best[f];
+        int bk = s_arg[f];
+        for (int s = 1; s < a.slices; ++s) {
+            const int k2 = s_arg[s * tj_nt + f];
+            if (k2 < 0) continue;
+            const Real b2 = s_best[s * tj_nt + f];
+            if (bk < 0 || b2 < best || (b2 == best && k2 < bk)) { best = b2; bk = k2; }
         }
-        const size_t o = (size_t)iv * plane + f;
-        a.J_out[o] = bu < 0 ? (Real)INFINITY : best;
-        if (MODE == 0) a.P_out[o] = bu;
+        const Real val = bk < 0 ? (Real)INFINITY : best;
+        a.J_out[obase + f] = val;
+        if (obase + f > 0) a.J_out1[obase + f - 1] = val;
+        a.P_out[obase + f] = bk < 0 ? -1 : u[bk];
+    }
+}
+
+// Terminal-field step over (v, soc) (field_sweep K:801-865): no time axis,
+// signals always green, stop-sign dwell charged at the time price (K:825).
+// One CTA per source plane; threads = slices x S (S >= n_soc).
+template <typename Real>
+__global__ void __launch_bounds__(1024)
+field_stage_kernel(StageArgs<Real> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int iv = blockIdx.x;
+    const int nx = a.nx;
+    const double v = a.v_src[iv];
+    const int count = (a.src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : a.count[iv];
+    const int S = a.S;
+    const int slice = threadIdx.x / S;
+    const int jx = threadIdx.x - slice * S;
+    Real* s_best = (Real*)smem;
+    int32_t* s_arg = (int32_t*)(smem + align16((size_t)a.slices * S * sizeof(Real)));
+    const bool hold = a.src_kind == ECO_NODE_STOP && v == 0.0;
+    const double wait_cost = hold ? (1.0 - a.gamma) * a.dwell : 0.0;
+    Real best = a.j_inf;
+    int bk = -1;
+    if (jx < nx) {
+        const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
+        const RowRec<Real>* rows = a.row + a.row_off[iv] + jx;
+        for (int k = slice; k < count; k += a.slices) {
+            const RowRec<Real> ro = rows[(size_t)k * nx];
+            if (ro.off < 0) continue;
+            const ActRec<Real> rc = acts[k];
+            const Real* b = a.J_next + ro.cell;
+            const int dv = (rc.meta & kRecDvh) ? nx : 0;     // next speed plane of G (v, soc)
+            const int dx = ro.wx > (Real)0 ? 1 : 0;
+            const Real lo = lerp(__ldg(b), __ldg(b + dv), rc.wv);                    // bilin2_abs K:335-337
+            const Real hi = lerp(__ldg(b + dx), __ldg(b + dv + dx), rc.wv);
+            const Real gn = lerp(lo, hi, ro.wx);
+            Real F;
+            if (hold) F = (Real)(a.c1d[(size_t)iv * a.U + k] + wait_cost) + gn;      // K:862
+            else F = rc.c1 + gn;
+            if (F < best) { best = F; bk = k; }
+        }
+    }
+    s_best[threadIdx.x] = best;
+    s_arg[threadIdx.x] = bk;
+    __syncthreads();
+    if (slice == 0 && jx < nx) {
+        for (int s = 1; s < a.slices; ++s) {
+            const int k2 = s_arg[s * S + jx];
+            if (k2 < 0) continue;
+            const Real b2 = s_best[s * S + jx];
+            if (bk < 0 || b2 < best) { best = b2; bk = k2; }
+        }
+        a.J_out[(size_t)iv * nx + jx] = bk < 0 ? (Real)INFINITY : best;
     }
 }
 

@@ -96,7 +96,7 @@ __device__ __forceinline__ Real terminal_value(double base, double soc, double t
 // s..s+h and the terminal level J_h.
 template <typename Real>
 __global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, int s, int h,
-                                   const double* field, Ladders lad, Real* Jh) {
+                                   const double* field, Ladders lad, Real* Jh, Real* Jh1) {
     if (st->status != 0) return;
     __shared__ double t_axis[1024];
     const double t = st->x[2];
@@ -118,7 +118,13 @@ __global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, i
         const int iv = (int)(i / plane);
         const int jx = (int)((i - iv * plane) / c.nt);
         const double base = (c.use_field && field) ? field[((size_t)(s + h) * c.nv + iv) * c.nx + jx] : 0.0;
-        Jh[i] = terminal_value<Real>(base, c.soc_axis[jx], c.soc_target, c.soc_weight, c.j_inf);
+        const Real val = terminal_value<Real>(base, c.soc_axis[jx], c.soc_target, c.soc_weight, c.j_inf);
+        Jh[i] = val;
+        if (i > 0) Jh1[i - 1] = val;      // shifted copy (see level_copy in eco_api.cu)
+    }
+    for (size_t i = (size_t)c.nv * plane - 1 + threadIdx.x; i < (size_t)c.nv * plane + 8; i += blockDim.x) {
+        Jh1[i] = (Real)INFINITY;
+        if (i >= (size_t)c.nv * plane) Jh[i] = (Real)INFINITY;
     }
 }
 

@@ -187,6 +187,67 @@ def _rows_to_steps(rows: np.ndarray) -> list:
         for r in rows]
 
 
+class MpcSession:
+    """A route-resident device solver (eco_session_*): geometry, terminal
+    field and loop buffers stay in HBM across runs, so repeated closed loops
+    and single receding-horizon steps pay no allocation or upload."""
+
+    def __init__(self, vehicle: Vehicle, route: Route, spat: SpatSchedule, *, gamma: float, grids: GridSpec,
+                 penalty: PenaltyConfig, horizon: int, backend: str, teleport: bool = True,
+                 use_terminal_field: bool = True):
+        self.route, self.grids = route, grids
+        self.use_terminal_field = use_terminal_field
+        self._rp = _abi.RoutePack(route, spat)
+        self._cfg, self._keep = _config(vehicle, grids, penalty, gamma, horizon, teleport, use_terminal_field,
+                                        backend)
+        self._plant = _abi.pack_plant(vehicle.pack())
+        self._h = C.c_void_p()
+        self._lib = _abi.lib()
+        _abi.check(self._lib.eco_session_create(C.byref(self._plant), C.byref(self._rp.c), C.byref(self._cfg),
+                                                C.byref(self._h)), "eco_session_create")
+        self.h2d_bytes = (C.sizeof(self._plant) + C.sizeof(self._cfg) + sum(
+            a.nbytes for a in (self._rp.v_min, self._rp.v_max, self._rp.grade, self._rp.cos_g, self._rp.sin_g,
+                               self._rp.kinds, self._rp.cycle, self._rp.offset, self._rp.nwin, self._rp.win,
+                               *self._keep)))
+
+    def fit(self, field: Optional[np.ndarray] = None, want_field: bool = True):
+        """Route geometry + terminal field on the device; returns (field or None, stats)."""
+        n = self.route.node_count
+        out = np.empty((n, self.grids.n_v, self.grids.n_soc)) if (want_field and self.use_terminal_field) else None
+        fin = None if field is None else np.ascontiguousarray(field, dtype=np.float64)
+        st = _abi.EcoStats()
+        _abi.check(self._lib.eco_session_fit(self._h, None if fin is None else _abi.ptr(fin, C.c_double),
+                                             None if out is None else _abi.ptr(out, C.c_double), C.byref(st)),
+                   "eco_session_fit")
+        return out, st.as_dict()
+
+    def run(self, x_start: StateVector, start_node: int = 0, max_steps: int = -1, *, count_live: bool = False,
+            time_sweeps: bool = True):
+        """Closed loop on the device -> (rows, status, status_node, final_state, stats)."""
+        rows = np.zeros(max(self.route.node_count - 1, 1), dtype=_abi.TRAJ_DTYPE)
+        x0 = np.array([x_start.v, x_start.soc, x_start.t], dtype=np.float64)
+        fin = np.zeros(3)
+        n_rows, status, node = C.c_int32(0), C.c_int32(0), C.c_int32(-1)
+        flags = (_abi.RUN_COUNT_LIVE if count_live else 0) | (_abi.RUN_TIME_SWEEPS if time_sweeps else 0)
+        st = _abi.EcoStats()
+        _abi.check(self._lib.eco_session_run(
+            self._h, start_node, max_steps, _abi.ptr(x0, C.c_double),
+            rows.ctypes.data_as(C.POINTER(_abi.EcoTrajRow)), C.byref(n_rows), C.byref(status), C.byref(node),
+            _abi.ptr(fin, C.c_double), flags, C.byref(st)), "eco_session_run")
+        return rows[:n_rows.value], status.value, node.value, fin, st.as_dict()
+
+    def close(self):
+        if self._h:
+            self._lib.eco_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def run_closed_loop(vehicle: Vehicle, route: Route, spat: SpatSchedule, x_start: StateVector, *,
                     gamma: float, grids: GridSpec, penalty: PenaltyConfig, horizon: int, backend: str,
                     teleport: bool = True, field: Optional[TerminalCostField] = None,
@@ -219,6 +280,17 @@ def run_closed_loop(vehicle: Vehicle, route: Route, spat: SpatSchedule, x_start:
     return rows[:n_rows.value], status.value, status_node.value, fin, field_out, st.as_dict()
 
 
+def _raise_step_status(status, rows, s, x, teleport):
+    if status == _abi.RUN_MISMATCH:
+        raise RuntimeError(f"solver/plant transition mismatch at node {s}")
+    if status == _abi.RUN_INFEASIBLE or (len(rows) and rows[0]["fallback"]):
+        raise StartStateInfeasibleError(
+            f"no admissible action from node {s} at v={x.v:.2f} m/s, soc={x.soc:.3f}, t={x.t:.1f} s "
+            f"(teleport={'on' if teleport else 'off'})")
+    if status != _abi.RUN_OK or not len(rows):
+        raise RuntimeError(f"plant step failed at node {s}")
+
+
 def mpc_step(vehicle: Vehicle, route: Route, spat: SpatSchedule, x: StateVector, s: int, *, gamma: float,
              grids: GridSpec, penalty: PenaltyConfig, horizon: int, terminal: Optional[TerminalCostField] = None,
              backend: str = "b200", workers: int = 8, teleport: bool = True, perturb_ties: bool = False):
@@ -234,14 +306,7 @@ def mpc_step(vehicle: Vehicle, route: Route, spat: SpatSchedule, x: StateVector,
     rows, status, _, fin, _, st = run_closed_loop(
         vehicle, route, spat, x, gamma=gamma, grids=grids, penalty=penalty, horizon=horizon, backend=backend,
         teleport=teleport, field=terminal, use_terminal_field=terminal is not None, start_node=s, max_steps=1)
-    if status == _abi.RUN_MISMATCH:
-        raise RuntimeError(f"solver/plant transition mismatch at node {s}")
-    if status == _abi.RUN_INFEASIBLE or (len(rows) and rows[0]["fallback"]):
-        raise StartStateInfeasibleError(
-            f"no admissible action from node {s} at v={x.v:.2f} m/s, soc={x.soc:.3f}, t={x.t:.1f} s "
-            f"(teleport={'on' if teleport else 'off'})")
-    if status != _abi.RUN_OK or not len(rows):
-        raise RuntimeError(f"plant step failed at node {s}")
+    _raise_step_status(status, rows, s, x, teleport)
     r = rows[0]
     return (ActionVector(t_eng=float(r["t_eng"]), t_bsg=float(r["t_bsg"])),
             MpcStepInfo(predicted_next=StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2])),
@@ -275,18 +340,27 @@ class EcoDrivingMPC:
             raise ValueError("horizon must be >= 1")
         self.route_ = route
         self.spat_ = spat
-        self.terminal_field_ = (build_terminal_cost(route, self.vehicle, gamma=self.gamma, grids=self.grids,
-                                                    penalty=self.penalty, spat=spat, backend=self.backend)
+        self.session_ = MpcSession(self.vehicle, route, spat, gamma=self.gamma, grids=self.grids,
+                                   penalty=self.penalty, horizon=self.horizon, backend=self.backend,
+                                   teleport=self.teleport, use_terminal_field=self.use_terminal_field)
+        values, self.fit_stats_ = self.session_.fit()
+        self.terminal_field_ = (TerminalCostField(values=values, route_name=route.name, gamma=self.gamma,
+                                                  grids=self.grids, penalty=self.penalty)
                                 if self.use_terminal_field else None)
         return self
 
     def control(self, x: StateVector, s: int) -> ControlDecision:
+        """One receding-horizon decision at (x, s) on the fitted session."""
         self._check_fitted()
-        action, info = mpc_step(self.vehicle, self.route_, self.spat_, x, s, gamma=self.gamma, grids=self.grids,
-                                penalty=self.penalty, horizon=self.horizon, terminal=self.terminal_field_,
-                                backend=self.backend, teleport=self.teleport, perturb_ties=self.perturb_ties)
-        return ControlDecision(action=action, predicted_next=info.predicted_next, cost_to_go=info.cost_to_go,
-                               solver_wall_s=info.solve_wall_s)
+        n = self.route_.node_count
+        if not 0 <= s < n - 1:
+            raise ValueError(f"start node {s} out of range for {n} route nodes")
+        rows, status, _, fin, st = self.session_.run(x, start_node=s, max_steps=1)
+        _raise_step_status(status, rows, s, x, self.teleport)
+        r = rows[0]
+        return ControlDecision(action=ActionVector(t_eng=float(r["t_eng"]), t_bsg=float(r["t_bsg"])),
+                               predicted_next=StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2])),
+                               cost_to_go=float(r["cost_to_go"]), solver_wall_s=st["device_ms"] / 1e3)
 
     def _check_fitted(self):
         if not hasattr(self, "route_"):
@@ -315,11 +389,9 @@ def simulate_closed_loop(route: Route, spat: SpatSchedule, controller: EcoDrivin
     if route.node_count == 1:
         traj.final_state = x_start
         return traj
-    rows, status, node, fin, _, st = run_closed_loop(
-        controller.vehicle, route, spat, x_start, gamma=controller.gamma, grids=controller.grids,
-        penalty=controller.penalty, horizon=controller.horizon, backend=controller.backend,
-        teleport=controller.teleport, field=controller.terminal_field_,
-        use_terminal_field=controller.use_terminal_field)
+    if route is not controller.route_:
+        raise ValueError("simulate_closed_loop: controller was fitted on a different route")
+    rows, status, node, fin, st = controller.session_.run(x_start)
     if status == _abi.RUN_MISMATCH:
         raise RuntimeError(f"solver/plant transition mismatch at node {node}")
     traj.steps = _rows_to_steps(rows)
