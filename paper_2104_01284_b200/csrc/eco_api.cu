@@ -154,6 +154,7 @@ struct Geometry {
     DBuf<RowRec<Real>> row;
     DBuf<RowRec2<Real>> row2;
     DBuf<TilePlan> tiles;
+    DBuf<int32_t> order;
     int h_gmax[4] = {0, 0, 0, 0};     // max feasible actions of a plane
     int64_t rows_total = 0;
     int tj = 0, nchunk = 0, band_cap = 0;   // stage-kernel tile shape the plans were built for
@@ -202,7 +203,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     ECO_CUDA(cudaGetLastError());
     // staging plans of the (v, soc, t) stage kernel's tiles
     const int upr = (g.nt + kZP - 1) / kZP;
-    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", std::max(1, 32 / upr))));
+    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", std::max(1, 16 / upr))));
     G.nchunk = (g.nx + G.tj - 1) / G.tj;
     G.band_cap = env_int("ECO_BAND_KB", 40) * 1024 / (int)sizeof(Real);
     const size_t ntiles = (size_t)npi * G.nchunk;
@@ -212,7 +213,10 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
         G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p);
     ECO_CUDA(cudaGetLastError());
-    if (launches) *launches += 5;
+    if (G.order.n != ntiles) G.order.alloc(ntiles);
+    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.tj, g.nx, G.order.p);
+    ECO_CUDA(cudaGetLastError());
+    if (launches) *launches += 6;
 }
 
 // Tile shape of the stage kernel: tj SoC rows x n_t, S threads per action
@@ -239,9 +243,10 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode) {
         t.tj = G.tj;
         t.nchunk = G.nchunk;
         const int upr = (nt + kZP - 1) / kZP;
-        const int per_row = (nt % 2 == 0) ? upr : nt;       // fast path: kZP states / thread
-        t.S = (t.tj * per_row + 31) / 32 * 32;
-        if (t.S > 512) t.S = 512;
+        // threads per action slice: one per kZP ladder states of the tile (a
+        // warp may hold two slices); the per-state path strides over states
+        const int per_row = (nt % 2 == 0) ? upr : nt;
+        t.S = std::min(512, t.tj * per_row);
         t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", std::max(1, 256 / t.S)), 512 / t.S));
         t.count_max = std::max(1, G.h_gmax[0]);
         t.band_cap = G.band_cap;
@@ -265,6 +270,7 @@ StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int n
     a.row = G.row.p;
     a.row2 = G.row2.p;
     a.tiles = G.tiles.p + (size_t)p * g.nv * G.nchunk;
+    a.order = G.order.p + (size_t)p * g.nv * G.nchunk;
     a.v_src = d_vsrc;
     a.nv = g.nv;
     a.nx = g.nx;
@@ -282,7 +288,18 @@ StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int n
 
 template <typename K>
 void set_smem_attr(K kernel, size_t smem) {
-    if (smem > 48 * 1024) ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // cached per kernel: keeps attribute calls out of stream capture
+    static thread_local std::vector<std::pair<const void*, size_t>> done;
+    if (smem <= 48 * 1024) return;
+    for (auto& d : done)
+        if (d.first == (const void*)kernel) {
+            if (d.second >= smem) return;
+            d.second = smem;
+            ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            return;
+        }
+    ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.emplace_back((const void*)kernel, smem);
 }
 
 template <typename Real, int MODE>
@@ -298,6 +315,57 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
         field_stage_kernel<Real><<<grid, block, tc.smem, st>>>(a);
     }
     ECO_CUDA(cudaGetLastError());
+}
+
+// Cooperative persistent launch of all stages of a solve (bellman_solve_kernel).
+struct SolveSync {
+    DBuf<unsigned> bar;
+    DBuf<int> tile_ctr;
+    void ensure(int H) {
+        if (!bar.p) {
+            bar.alloc(2);
+            ECO_CUDA(cudaMemset(bar.p, 0, 2 * sizeof(unsigned)));
+        }
+        if (tile_ctr.n < (size_t)H) tile_ctr.alloc(H);
+    }
+};
+
+inline int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        ECO_CUDA(cudaGetDevice(&dev));
+        ECO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+template <typename Real>
+void launch_solve(SolveArgs<Real>& sa, const TileCfg& tc, bool count, SolveSync& sync, cudaStream_t st) {
+    sync.ensure(sa.H);
+    sa.bar = sync.bar.p;
+    sa.tile_ctr = sync.tile_ctr.p;
+    ECO_CUDA(cudaMemsetAsync(sync.tile_ctr.p, 0, sa.H * sizeof(int), st));
+    const int block = tc.S * tc.slices;
+    auto k = count ? bellman_solve_kernel<Real, true> : bellman_solve_kernel<Real, false>;
+    set_smem_attr(k, tc.smem);
+    int per_sm = 0;
+    ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, tc.smem));
+    if (per_sm < 1) throw ArgError{"solve kernel does not fit on an SM"};
+    const int grid = std::min(per_sm * sm_count(), std::max(1, sa.ntiles));
+    void* args[] = {&sa};
+    ECO_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(block), args, tc.smem, st));
+}
+
+template <typename Real>
+SolveArgs<Real> solve_args(Geometry<Real>& G, const TileCfg& tc, int nt) {
+    SolveArgs<Real> sa{};
+    sa.base = stage_args(G, 0, nullptr, nt, tc);
+    sa.pair_stride = (size_t)G.dims.nv * G.dims.U;
+    sa.plane_stride = G.dims.nv;
+    sa.tile_stride = G.dims.nv * G.nchunk;
+    sa.ntiles = G.dims.nv * G.nchunk;
+    return sa;
 }
 
 void check_problem(const EcoProblem* pr) {
@@ -418,8 +486,61 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     }
     std::vector<TileCfg> tcs(H);
     for (int k = 0; k < H; ++k) tcs[k] = tile_cfg(tabs ? toyG[k] : G, nt, 0);
+    std::vector<int8_t> hkinds(H);
+    for (int k = 0; k < H; ++k) hkinds[k] = (int8_t)plans[k].src_kind;
+    DBuf<int8_t> d_kinds(H);
+    d_kinds.upload(hkinds.data(), H, st);
+    SolveSync ssync;
+    const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0;
     sweep.start(st);
-    for (int k = H - 1; k >= 0; --k) {
+    if (persistent) {
+        SolveArgs<Real> sa = solve_args(G, tcs[0], nt);
+        sa.base.live = count ? d_live.p : nullptr;
+        sa.base.t0 = pr->t0;
+        sa.base.dtg = pr->dtg;
+        sa.base.j_inf = (Real)pr->j_inf;
+        sa.vaxes = d_v.p;
+        sa.src_kinds = d_kinds.p;
+        sa.plan0 = 0;
+        sa.H = H;
+        sa.green_shift = 0;
+        sa.green = d_green.p; sa.dep_ok = d_dep.p; sa.t_dep = d_tdep.p; sa.wait = d_wait.p;
+        sa.J = d_J.p; sa.LV = LV; sa.LC = LC;
+        sa.P = d_P.p; sa.PV = ns;
+        DBuf<unsigned long long> dbgbuf;
+        const bool dbg_on = env_int("ECO_DEBUG_SOLVE", 0) != 0;
+        if (dbg_on) {
+            dbgbuf.alloc((size_t)4 * H * 2048);
+            ECO_CUDA(cudaMemsetAsync(dbgbuf.p, 0, dbgbuf.n * 8, st));
+            sa.base.dbg = dbgbuf.p;
+        }
+        launch_solve(sa, tcs[0], count, ssync, st);
+        ++launches;
+        if (dbg_on) {
+            std::vector<unsigned long long> h(dbgbuf.n);
+            dbgbuf.download(h.data(), h.size(), st);
+            ECO_CUDA(cudaStreamSynchronize(st));
+            int nb = 0;
+            while (nb < 2048 && h[(size_t)nb * 4 * H + 4 * (H - 1)]) ++nb;
+            unsigned long long t0 = ~0ull;
+            for (int b = 0; b < nb; ++b) t0 = std::min(t0, h[(size_t)b * 4 * H + 4 * (H - 1)]);
+            for (int k = H - 1; k >= 0; --k) {
+                double s0 = 1e30, e_min = 1e30, e_max = 0, b_max = 0, nt_max = 0, nt_min = 1e9;
+                for (int b = 0; b < nb; ++b) {
+                    const unsigned long long* d = &h[(size_t)b * 4 * H + 4 * k];
+                    s0 = std::min(s0, (d[0] - t0) / 1e3);
+                    const double e = (d[1] - t0) / 1e3;
+                    e_min = std::min(e_min, e); e_max = std::max(e_max, e);
+                    if (d[2]) b_max = std::max(b_max, (d[2] - t0) / 1e3);
+                    nt_max = std::max(nt_max, (double)d[3]); nt_min = std::min(nt_min, (double)d[3]);
+                }
+                std::fprintf(stderr, "stage %2d start %8.2f tiles-done min %8.2f max %8.2f barrier-out %8.2f tiles/cta %.0f..%.0f\n",
+                             k, s0, e_min, e_max, b_max, nt_min, nt_max);
+            }
+            std::fprintf(stderr, "grid %d ctas\n", nb);
+        }
+    }
+    for (int k = H - 1; k >= 0 && !persistent; --k) {
         const TileCfg& tc = tcs[k];
         StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, d_v.p + (size_t)k * nv, nt, tc)
                                  : stage_args(G, k, d_v.p + (size_t)k * nv, nt, tc);
@@ -437,7 +558,28 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         a.t0 = pr->t0;
         a.dtg = pr->dtg;
         a.j_inf = (Real)pr->j_inf;
+        DBuf<unsigned long long> dbgbuf;
+        const bool dbg_on = env_int("ECO_DEBUG_STAGE", 0) != 0;
+        if (dbg_on) {
+            dbgbuf.alloc((size_t)6 * nv * tc.nchunk);
+            ECO_CUDA(cudaMemsetAsync(dbgbuf.p, 0, dbgbuf.n * 8, st));
+            a.dbg = dbgbuf.p;
+        }
         launch_stage<Real, 0>(a, tc, count, st);
+        if (dbg_on) {
+            std::vector<unsigned long long> h(dbgbuf.n);
+            dbgbuf.download(h.data(), h.size(), st);
+            ECO_CUDA(cudaStreamSynchronize(st));
+            const int nb = nv * tc.nchunk;
+            unsigned long long t0 = ~0ull, t1 = 0;
+            for (int b = 0; b < nb; ++b) { t0 = std::min(t0, h[6 * b]); t1 = std::max(t1, h[6 * b + 3]); }
+            std::fprintf(stderr, "stage k=%d ctas=%d span=%.2fus\n", k, nb, (t1 - t0) / 1e3);
+            for (int b = 0; b < nb; ++b)
+                std::fprintf(stderr, "  cta %3d sm %3llu path %llu work %5llu start %7.2f staged %7.2f looped %7.2f end %7.2f\n",
+                             b, h[6 * b + 4] & 0xFFFF, h[6 * b + 4] >> 16, h[6 * b + 5], (h[6 * b] - t0) / 1e3,
+                             h[6 * b + 1] ? (h[6 * b + 1] - t0) / 1e3 : -1.0, (h[6 * b + 2] - t0) / 1e3,
+                             (h[6 * b + 3] - t0) / 1e3);
+        }
         ++launches;
     }
     sweep.stop(st);
@@ -676,7 +818,12 @@ struct Session : SessionBase {
     DBuf<EcoTrajRow> rows;
     DBuf<unsigned long long> live;
     std::vector<cudaEvent_t> ev;
+    SolveSync ssync;
     cudaStream_t st = 0;
+    // CUDA graph of a whole closed loop (prepare / H stage sweeps / decide per
+    // node), captured on first use and replayed: no per-kernel launch gaps
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<long long> gkey;
 
     Session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
         cfg = *c;
@@ -702,9 +849,14 @@ struct Session : SessionBase {
         ev.resize(2 * (size_t)n);
         for (auto& e : ev) ECO_CUDA(cudaEventCreate(&e));
         ECO_CUDA(cudaStreamSynchronize(st));
+        // a blocking stream of its own (stream capture is impossible on the
+        // legacy default stream; blocking keeps it ordered with stream 0)
+        ECO_CUDA(cudaStreamCreate(&st));
     }
     ~Session() override {
         for (auto& e : ev) cudaEventDestroy(e);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (st) cudaStreamDestroy(st);
     }
 
     void fit(const double* field_in, double* field_out, EcoStats* stats) override {
@@ -747,52 +899,105 @@ struct Session : SessionBase {
         LoopState h0{};
         h0.x[0] = x0[0]; h0.x[1] = x0[1]; h0.x[2] = x0[2];
         EventTimer all;
-        all.start(st);
-        state.upload(&h0, 1, st);
-        if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
         Ladders lad{green.p, dep.p, tdep.p, wait.p, tax.p};
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
         const TileCfg tc = tile_cfg(ctx.G, nt, 0);
+        const bool persistent = env_int("ECO_PERSISTENT", 0) != 0;
         int64_t stages = 0;
         int nev = 0;
-        for (int s = start_node; s < s_end; ++s) {
-            const int h = H < n - 1 - s ? H : n - 1 - s;
-            const size_t LV = level_stride(ns), LC = level_copy(ns);
-            mpc_prepare_kernel<Real><<<1, 256, 0, st>>>(ctx.R.view, lc, state.p, s, h,
-                                                        cfg.use_terminal_field ? field.p : nullptr, lad,
-                                                        J.p + (size_t)h * LV, J.p + (size_t)h * LV + LC);
-            ECO_CUDA(cudaGetLastError());
-            ++launches;
-            if (timed) ECO_CUDA(cudaEventRecord(ev[2 * nev], st));
-            for (int k = h - 1; k >= 0; --k) {
-                StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tc);
-                a.green = green.p + (size_t)(k + 1) * nt;
-                a.dep_ok = dep.p + (size_t)k * nt;
-                a.t_dep = tdep.p + (size_t)k * nt;
-                a.wait = wait.p + (size_t)k * nt;
-                a.J_next = J.p + (size_t)(k + 1) * LV;
-                a.J_next1 = a.J_next + LC;
-                a.J_out = J.p + (size_t)k * LV;
-                a.J_out1 = a.J_out + LC;
-                a.P_out = P.p;
-                a.status = &state.p->status;
-                a.live = count ? live.p : nullptr;
-                a.src_kind = kinds[s + k];
-                a.t0_dev = tax.p;   // ladder origin depends on the device-resident clock
-                a.dtg = cfg.dt;
-                a.j_inf = (Real)cfg.j_inf;
-                launch_stage<Real, 0>(a, tc, count, st);
+        auto enqueue = [&](cudaStream_t qs, bool capturing) {
+            // inside a graph, events are recorded as external event nodes so
+            // cudaEventElapsedTime works on them after each replay
+            const unsigned evflag = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+            stages = 0;
+            nev = 0;
+            launches = 0;
+            for (int s = start_node; s < s_end; ++s) {
+                const int h = H < n - 1 - s ? H : n - 1 - s;
+                const size_t LV = level_stride(ns), LC = level_copy(ns);
+                mpc_prepare_kernel<Real><<<std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256)), 256, 0, qs>>>(
+                    ctx.R.view, lc, state.p, s, h, cfg.use_terminal_field ? field.p : nullptr, lad,
+                    J.p + (size_t)h * LV, J.p + (size_t)h * LV + LC);
+                ECO_CUDA(cudaGetLastError());
                 ++launches;
-                ++stages;
+                if (timed) ECO_CUDA(cudaEventRecordWithFlags(ev[2 * nev], qs, evflag));
+                if (persistent) {
+                    SolveArgs<Real> sa = solve_args(ctx.G, tc, nt);
+                    sa.base.status = &state.p->status;
+                    sa.base.live = count ? live.p : nullptr;
+                    sa.base.t0_dev = tax.p;
+                    sa.base.dtg = cfg.dt;
+                    sa.base.j_inf = (Real)cfg.j_inf;
+                    sa.vaxes = ctx.R.vaxes.p;
+                    sa.src_kinds = ctx.R.kinds.p;
+                    sa.plan0 = s;
+                    sa.H = h;
+                    sa.green_shift = 1;
+                    sa.green = green.p; sa.dep_ok = dep.p; sa.t_dep = tdep.p; sa.wait = wait.p;
+                    sa.J = J.p; sa.LV = LV; sa.LC = LC;
+                    sa.P = P.p; sa.PV = 0;
+                    launch_solve(sa, tc, count, ssync, qs);
+                    ++launches;
+                    stages += h;
+                }
+                for (int k = h - 1; k >= 0 && !persistent; --k) {
+                    StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tc);
+                    a.green = green.p + (size_t)(k + 1) * nt;
+                    a.dep_ok = dep.p + (size_t)k * nt;
+                    a.t_dep = tdep.p + (size_t)k * nt;
+                    a.wait = wait.p + (size_t)k * nt;
+                    a.J_next = J.p + (size_t)(k + 1) * LV;
+                    a.J_next1 = a.J_next + LC;
+                    a.J_out = J.p + (size_t)k * LV;
+                    a.J_out1 = a.J_out + LC;
+                    a.P_out = P.p;
+                    a.status = &state.p->status;
+                    a.live = count ? live.p : nullptr;
+                    a.src_kind = kinds[s + k];
+                    a.t0_dev = tax.p;   // ladder origin depends on the device-resident clock
+                    a.dtg = cfg.dt;
+                    a.j_inf = (Real)cfg.j_inf;
+                    launch_stage<Real, 0>(a, tc, count, qs);
+                    ++launches;
+                    ++stages;
+                }
+                if (timed) ECO_CUDA(cudaEventRecordWithFlags(ev[2 * nev + 1], qs, evflag));
+                ++nev;
+                mpc_decide_kernel<Real><<<1, kDecideThreads, 0, qs>>>(ctx.plant.p, ctx.R.view, lc, state.p, s, h,
+                                                                      lad, J.p + LV, rows.p);
+                ECO_CUDA(cudaGetLastError());
+                ++launches;
             }
-            if (timed) ECO_CUDA(cudaEventRecord(ev[2 * nev + 1], st));
-            ++nev;
-            mpc_decide_kernel<Real><<<1, kDecideThreads, 0, st>>>(ctx.plant.p, ctx.R.view, lc, state.p, s, h, lad,
-                                                                  J.p + LV, rows.p);
-            ECO_CUDA(cudaGetLastError());
-            ++launches;
+        };
+        const bool use_graph = !count && !persistent && env_int("ECO_GRAPH", 1) != 0;
+        if (use_graph) {
+            const std::vector<long long> key = {start_node, s_end, timed ? 1 : 0, (long long)(size_t)ctx.G.row2.p,
+                                                (long long)(size_t)ctx.G.tiles.p, (long long)(size_t)ctx.G.order.p,
+                                                (long long)(size_t)field.p, tc.tj, tc.slices};
+            if (!gexec || key != gkey) {
+                if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+                cudaGraph_t graph;
+                ECO_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                enqueue(st, true);
+                ECO_CUDA(cudaStreamEndCapture(st, &graph));
+                ECO_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+                cudaGraphDestroy(graph);
+                gkey = key;
+            }
+            // counters of the captured loop (same structure every replay)
+            stages = 0; nev = 0;
+            for (int s = start_node; s < s_end; ++s) { stages += H < n - 1 - s ? H : n - 1 - s; ++nev; }
+            launches = (int64_t)nev * 2 + stages;
+            all.start(st);
+            state.upload(&h0, 1, st);
+            ECO_CUDA(cudaGraphLaunch(gexec, st));
+        } else {
+            all.start(st);
+            state.upload(&h0, 1, st);
+            if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
+            enqueue(st, false);
         }
         all.stop(st);
         LoopState hs{};

@@ -333,6 +333,25 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
     }
 }
 
+// per plan: tiles sorted by descending work (count * rows), ties by index
+__global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int tj, int nx,
+                                  int32_t* __restrict__ order) {
+    const int p = blockIdx.x;
+    const int nt_ = nv * nchunk;
+    const int32_t* c = count + (size_t)p * nv;
+    for (int i = threadIdx.x; i < nt_; i += blockDim.x) {
+        const int iv = i / nchunk, ch = i - iv * nchunk;
+        const long w = (long)c[iv] * min(tj, nx - ch * tj);
+        int rank = 0;
+        for (int j = 0; j < nt_; ++j) {
+            const int jv = j / nchunk, jch = j - jv * nchunk;
+            const long wj = (long)c[jv] * min(tj, nx - jch * tj);
+            rank += (wj > w) || (wj == w && j < i);
+        }
+        order[(size_t)p * nt_ + rank] = i;
+    }
+}
+
 // ---------------------------------------------------------- stage sweep
 // Internal cost-to-go representation: +inf marks infeasible (the reference's
 // j_inf).  A gather touching an infeasible corner then yields inf or NaN and
@@ -349,6 +368,8 @@ struct StageArgs {
     const RowRec<Real>* row;      // compact (absolute)
     const RowRec2<Real>* row2;    // staged-path row records (same indexing as row)
     const TilePlan* tiles;        // [nv][nchunk] of this stage's plan
+    const int32_t* order;         // [nv * nchunk] tile launch order (heaviest first), nullable
+    unsigned long long* dbg;      // debug: per CTA {start, staged, looped, end, smid|path<<16, count} (nullable)
     const double* v_src;
     // ladders (n_t): destination green mask, source standstill arrays
     const uint8_t* green;
@@ -418,6 +439,16 @@ __device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 
 template <typename Real>
 struct TileSmem {
@@ -446,13 +477,15 @@ struct TileSmem {
 // 64-bit load.  Standstill planes (v == 0: red-wait / dwell relocation,
 // K:519-535) run a per-state loop.
 template <typename Real, bool COUNT>
-__global__ void __launch_bounds__(512)
-bellman_stage_kernel(StageArgs<Real> a) {
-    if (a.status && *a.status != 0) return;
-    extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
-    const int iv = blockIdx.x / a.nchunk;
-    const int j0 = (blockIdx.x - iv * a.nchunk) * a.tj;
+    unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
+    if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
+    // tiles are visited heaviest first (tile_order)
+    const int tile = a.order ? a.order[rank] : rank;
+    const int iv = tile / a.nchunk;
+    const int chunk = tile - iv * a.nchunk;
+    const int j0 = chunk * a.tj;
     const int nt = a.nt, nx = a.nx;
     const int tja = min(a.tj, nx - j0);
     const int plane = nx * nt;
@@ -494,7 +527,6 @@ bellman_stage_kernel(StageArgs<Real> a) {
     unsigned long long nlive = 0;
 
     const bool fast = v > 0.0 || !any_hold;
-    const int chunk = blockIdx.x - iv * a.nchunk;
     const TilePlan* tp = a.tiles ? a.tiles + (size_t)iv * a.nchunk + chunk : nullptr;
     const int nseg = tp ? tp->nseg : -1;
     Real* s_band = (Real*)(smem + L.band);
@@ -531,6 +563,7 @@ bellman_stage_kernel(StageArgs<Real> a) {
             cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
         cp_async_wait_all();
         __syncthreads();
+        if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
         // ---------------- staged fast path: corners from shared memory
         using PR = Pair<Real>;
         const int upr = (nt + kZP - 1) / kZP;
@@ -739,6 +772,11 @@ bellman_stage_kernel(StageArgs<Real> a) {
         if ((threadIdx.x & 31) == 0 && w) atomicAdd(a.live, w);
     }
     __syncthreads();
+    if (dbg && threadIdx.x == 0) {
+        dbg[2] = gtimer();
+        dbg[4] = smid() | ((unsigned long long)((fast ? 1 : 0) + (nseg >= 0 ? 2 : 0)) << 16);
+        dbg[5] = (unsigned long long)count * tja;
+    }
     // ---- merge slices: lexicographic (F, k); k ascends with the flat index
     const int32_t* u = a.u + (size_t)iv * a.U;
     for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
@@ -755,6 +793,19 @@ bellman_stage_kernel(StageArgs<Real> a) {
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
         a.P_out[obase + f] = bk < 0 ? -1 : u[bk];
     }
+    if (dbg) {
+        __syncthreads();
+        if (threadIdx.x == 0) dbg[3] = gtimer();
+    }
+    __syncthreads();      // shared buffers are reused by the caller's next tile
+}
+
+template <typename Real, bool COUNT>
+__global__ void __launch_bounds__(512)
+bellman_stage_kernel(StageArgs<Real> a) {
+    if (a.status && *a.status != 0) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    stage_tile<Real, COUNT>(a, blockIdx.x, smem);
 }
 
 // Terminal-field step over (v, soc) (field_sweep K:801-865): no time axis,
@@ -807,6 +858,111 @@ field_stage_kernel(StageArgs<Real> a) {
             if (bk < 0 || b2 < best) { best = b2; bk = k2; }
         }
         a.J_out[(size_t)iv * nx + jx] = bk < 0 ? (Real)INFINITY : best;
+    }
+}
+
+}  // namespace eco
+
+namespace eco {
+
+// =====================================================================
+// Persistent horizon solve (K2): one cooperative launch runs all H Bellman
+// stages (solve_horizon's loop dp.py:446-450) with a grid barrier between
+// consecutive stages; CTAs pull tiles of the current stage heaviest-first
+// from an atomic counter, so no launch gap sits between stages and the
+// per-stage load imbalance is absorbed dynamically.
+// =====================================================================
+template <typename Real>
+struct SolveArgs {
+    StageArgs<Real> base;         // plan-0 geometry pointers, dims, tile shape, scalars
+    size_t pair_stride;           // nv * U      (u, dt, c1d, act)
+    int plane_stride;             // nv          (count, row_off)
+    int tile_stride;              // nv * nchunk (tiles, order)
+    const double* vaxes;          // [P][nv] source speed axes
+    const int8_t* src_kinds;      // [P]
+    int plan0, H, ntiles;
+    int green_shift;              // 1: ladders are [H+1][nt] node arrays (stage k reads green k+1)
+    const uint8_t* green;
+    const uint8_t* dep_ok;
+    const double* t_dep;
+    const double* wait;
+    Real* J;                      // level k at J + k * LV (copy 0) and + LC (copy 1)
+    size_t LV, LC;
+    int32_t* P;                   // level k at P + k * PV
+    size_t PV;
+    unsigned* bar;                // [2]: arrivals, generation
+    int* tile_ctr;                // [H]
+};
+
+// generation barrier over the (co-resident, cooperative-launched) grid
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = bar + 1;
+        const unsigned gen = *vgen;
+        __threadfence();
+        if (atomicAdd(&bar[0], 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(&bar[1], 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename Real>
+__device__ __forceinline__ StageArgs<Real> stage_of(const SolveArgs<Real>& sa, int k) {
+    StageArgs<Real> a = sa.base;
+    const int p = sa.plan0 + k;
+    a.count += (size_t)p * sa.plane_stride;
+    a.row_off += (size_t)p * sa.plane_stride;
+    a.u += (size_t)p * sa.pair_stride;
+    a.dt += (size_t)p * sa.pair_stride;
+    a.c1d += (size_t)p * sa.pair_stride;
+    a.act += (size_t)p * sa.pair_stride;
+    a.tiles += (size_t)p * sa.tile_stride;
+    a.order += (size_t)p * sa.tile_stride;
+    a.v_src = sa.vaxes + (size_t)p * a.nv;
+    a.src_kind = sa.src_kinds[p];
+    a.green = sa.green + (size_t)(k + sa.green_shift) * a.nt;
+    a.dep_ok = sa.dep_ok + (size_t)k * a.nt;
+    a.t_dep = sa.t_dep + (size_t)k * a.nt;
+    a.wait = sa.wait + (size_t)k * a.nt;
+    a.J_next = sa.J + (size_t)(k + 1) * sa.LV;
+    a.J_next1 = a.J_next + sa.LC;
+    a.J_out = sa.J + (size_t)k * sa.LV;
+    a.J_out1 = a.J_out + sa.LC;
+    a.P_out = sa.P + (size_t)k * sa.PV;
+    return a;
+}
+
+template <typename Real, bool COUNT>
+__global__ void __launch_bounds__(512)
+bellman_solve_kernel(SolveArgs<Real> sa) {
+    if (sa.base.status && *sa.base.status != 0) return;    // same value for every CTA
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_rank;
+    unsigned long long* dbg = sa.base.dbg ? sa.base.dbg + (size_t)blockIdx.x * 4 * sa.H : nullptr;
+    for (int k = sa.H - 1; k >= 0; --k) {
+        StageArgs<Real> a = stage_of(sa, k);
+        a.dbg = nullptr;
+        int ntile = 0;
+        if (dbg && threadIdx.x == 0) dbg[4 * k] = gtimer();
+        for (;;) {
+            if (threadIdx.x == 0) s_rank = atomicAdd(&sa.tile_ctr[k], 1);
+            __syncthreads();
+            const int rank = s_rank;
+            __syncthreads();
+            if (rank >= sa.ntiles) break;
+            stage_tile<Real, COUNT>(a, rank, smem);
+            ++ntile;
+        }
+        if (dbg && threadIdx.x == 0) { dbg[4 * k + 1] = gtimer(); dbg[4 * k + 3] = ntile; }
+        if (k > 0) grid_barrier(sa.bar, gridDim.x);
+        if (dbg && threadIdx.x == 0) dbg[4 * k + 2] = gtimer();
     }
 }
 

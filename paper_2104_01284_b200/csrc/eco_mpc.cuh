@@ -92,40 +92,46 @@ __device__ __forceinline__ Real terminal_value(double base, double soc, double t
     return val >= j_inf ? (Real)INFINITY : (Real)val;
 }
 
-// One block.  Builds the time ladder at x.t, the node ladders of nodes
-// s..s+h and the terminal level J_h.
+// Builds the time ladder at x.t, the node ladders of nodes s..s+h (block 0)
+// and the terminal level J_h (all blocks; grid-stride over (v, soc) cells,
+// each replicated along t, both level copies).
 template <typename Real>
 __global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, int s, int h,
                                    const double* field, Ladders lad, Real* Jh, Real* Jh1) {
     if (st->status != 0) return;
-    __shared__ double t_axis[1024];
     const double t = st->x[2];
     const double t0 = c.dt * floor(t / c.dt);          // GridSpec.t_axis dp.py:75-77
-    for (int z = threadIdx.x; z < c.nt; z += blockDim.x) {
-        const double tz = t0 + c.dt * (double)z;
-        lad.t_axis[z] = tz;
-        if (z < 1024) t_axis[z] = tz;
+    const int nt = c.nt;
+    if (blockIdx.x == 0) {
+        __shared__ double t_axis[1024];
+        for (int z = threadIdx.x; z < nt; z += blockDim.x) {
+            const double tz = t0 + c.dt * (double)z;
+            lad.t_axis[z] = tz;
+            if (z < 1024) t_axis[z] = tz;
+        }
+        __syncthreads();
+        const double* tax = nt <= 1024 ? t_axis : lad.t_axis;
+        for (int i = threadIdx.x; i < (h + 1) * nt; i += blockDim.x) {
+            const int k = i / nt, z = i - k * nt;
+            node_ladder(r, s + k, tax, nt, c.teleport, lad.green + k * nt, lad.dep_ok + k * nt,
+                        lad.t_dep + k * nt, lad.wait + k * nt, z);
+        }
     }
-    __syncthreads();
-    const double* tax = c.nt <= 1024 ? t_axis : lad.t_axis;
-    for (int i = threadIdx.x; i < (h + 1) * c.nt; i += blockDim.x) {
-        const int k = i / c.nt, z = i - k * c.nt;
-        node_ladder(r, s + k, tax, c.nt, c.teleport, lad.green + (size_t)k * c.nt, lad.dep_ok + (size_t)k * c.nt,
-                    lad.t_dep + (size_t)k * c.nt, lad.wait + (size_t)k * c.nt, z);
-    }
-    const size_t plane = (size_t)c.nx * c.nt;
-    for (size_t i = threadIdx.x; i < (size_t)c.nv * plane; i += blockDim.x) {
-        const int iv = (int)(i / plane);
-        const int jx = (int)((i - iv * plane) / c.nt);
-        const double base = (c.use_field && field) ? field[((size_t)(s + h) * c.nv + iv) * c.nx + jx] : 0.0;
+    const int ncell = c.nv * c.nx;
+    const int total = ncell * nt;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int cell = i / nt;
+        const int jx = cell - (cell / c.nx) * c.nx;
+        const double base = (c.use_field && field) ? field[(size_t)(s + h) * ncell + cell] : 0.0;
         const Real val = terminal_value<Real>(base, c.soc_axis[jx], c.soc_target, c.soc_weight, c.j_inf);
         Jh[i] = val;
         if (i > 0) Jh1[i - 1] = val;      // shifted copy (see level_copy in eco_api.cu)
     }
-    for (size_t i = (size_t)c.nv * plane - 1 + threadIdx.x; i < (size_t)c.nv * plane + 8; i += blockDim.x) {
-        Jh1[i] = (Real)INFINITY;
-        if (i >= (size_t)c.nv * plane) Jh[i] = (Real)INFINITY;
-    }
+    if (blockIdx.x == 0)
+        for (int i = total - 1 + threadIdx.x; i < total + 8; i += blockDim.x) {
+            Jh1[i] = (Real)INFINITY;
+            if (i >= total) Jh[i] = (Real)INFINITY;
+        }
 }
 
 // interp3_abs (K:340-361) on an internal table at a continuous query,

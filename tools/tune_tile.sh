@@ -1,6 +1,6 @@
 #!/bin/bash
 # Per-stage sweep time of the C2 workload for several tile shapes / band caps.
-for cfg in "4 8 40" "4 16 40" "4 4 40" "8 4 64" "8 8 64" "2 8 24" "2 16 24" "4 8 24" "13 2 96"; do
+for cfg in "2 16 32" "4 16 40" "2 8 32"; do
   set -- $cfg
   ECO_TILE_TJ=$1 ECO_TILE_SLICES=$2 ECO_BAND_KB=$3 python tools/profile_c2.py --steps 20 > /tmp/t.log 2>&1
   python3 - "$1" "$2" "$3" <<'PY'
