@@ -388,21 +388,15 @@ class SolveResult:
         return self.tables[0]
 
 
-def solve_horizon(ctx: SolveContext, x_start: Optional[StateVector] = None, *, backend: str = "b200",
-                  workers: int = 8, perturb_ties: bool = False, count_live: bool = False) -> SolveResult:
-    """Backward recursion over the whole horizon on the device (dp.py:425-475).
-
-    All H stages run back to back on the GPU from one upload of the context;
-    the full J / P stacks come back in the reference's layout."""
+def solve_stacks(ctx, backend: str = "b200", count_live: bool = False):
+    """Device solve of a context -> (J stack (H+1, n_v, n_soc, n_t) f64,
+    P stack (H, ...) int32, stats).  ``ctx`` only needs the reference
+    SolveContext's attributes (dp.py:191-214), so this also serves the
+    reference's own objects (see plugin.py)."""
     prec = precision_of(backend)
-    if perturb_ties:
-        raise ValueError("perturb_ties is a CPU-backend debug aid; the B200 kernels keep the lowest-index rule")
     g, H = ctx.grids, ctx.horizon
-    j_inf = ctx.penalty.j_inf
-    t0 = time.perf_counter()
     m = _Marshal(ctx, ctx.steps)
     terminal = _f64(ctx.terminal)
-    ns = g.n_v * g.n_soc * g.n_t
     J_stack = np.empty((H + 1, g.n_v, g.n_soc, g.n_t))
     P_stack = np.empty((H, g.n_v, g.n_soc, g.n_t), dtype=np.int32)
     st = _abi.EcoStats()
@@ -410,8 +404,23 @@ def solve_horizon(ctx: SolveContext, x_start: Optional[StateVector] = None, *, b
         C.byref(m.plant), C.byref(m.prob), m.plans, H, _abi.ptr(terminal, C.c_double),
         _abi.ptr(J_stack, C.c_double), _abi.ptr(P_stack, C.c_int32), prec, int(count_live), C.byref(st)),
         "eco_solve_horizon")
+    return J_stack, P_stack, st.as_dict()
+
+
+def solve_horizon(ctx: SolveContext, x_start: Optional[StateVector] = None, *, backend: str = "b200",
+                  workers: int = 8, perturb_ties: bool = False, count_live: bool = False) -> SolveResult:
+    """Backward recursion over the whole horizon on the device (dp.py:425-475).
+
+    All H stages run back to back on the GPU from one upload of the context;
+    the full J / P stacks come back in the reference's layout."""
+    precision_of(backend)
+    if perturb_ties:
+        raise ValueError("perturb_ties is a CPU-backend debug aid; the B200 kernels keep the lowest-index rule")
+    H = ctx.horizon
+    j_inf = ctx.penalty.j_inf
+    t0 = time.perf_counter()
+    J_stack, P_stack, stats = solve_stacks(ctx, backend, count_live)
     wall = time.perf_counter() - t0
-    assert J_stack.size == (H + 1) * ns
     tables = [CostToGoTable(values=J_stack[k], v_axis=ctx.v_axes[k], soc_axis=ctx.soc_axis,
                             t_axis=ctx.t_axis, j_inf=j_inf) for k in range(H + 1)]
     policies = [PolicyTable(values=P_stack[k], te_axis=ctx.te_axis, tb_axis=ctx.tb_axis) for k in range(H)]
@@ -423,7 +432,7 @@ def solve_horizon(ctx: SolveContext, x_start: Optional[StateVector] = None, *, b
                 f"no feasible continuation from node {ctx.s} at v={x_start.v:.2f} m/s, "
                 f"soc={x_start.soc:.3f}, t={x_start.t:.1f} s")
     return SolveResult(s=ctx.s, horizon=H, t_start=ctx.t_start, backend=backend, cost_at_start=cost0,
-                       tables=tables, policies=policies, wall_time_s=wall, stats=st.as_dict())
+                       tables=tables, policies=policies, wall_time_s=wall, stats=stats)
 
 
 # ------------------------------------------------------------- toy instances

@@ -314,6 +314,31 @@ def mpc_step(vehicle: Vehicle, route: Route, spat: SpatSchedule, x: StateVector,
                         solve_wall_s=st["device_ms"] / 1e3, horizon=h))
 
 
+_SESSIONS: "dict" = {}
+_SESSION_CAP = 4
+
+
+def _session_for(vehicle, route, spat, **kw) -> "MpcSession":
+    """Device sessions are cached per (vehicle, route, SPaT, settings): a
+    re-fit on the same route reuses the HBM-resident buffers and the captured
+    closed-loop graph instead of reallocating them (the cache keeps the keyed
+    objects alive, so their ids stay unique)."""
+    key = (id(vehicle), id(route), id(spat)) + tuple(sorted(kw.items()))
+    hit = _SESSIONS.get(key)
+    if hit is not None:
+        return hit[0]
+    while len(_SESSIONS) >= _SESSION_CAP:
+        _SESSIONS.pop(next(iter(_SESSIONS)))[0].close()
+    sess = MpcSession(vehicle, route, spat, **kw)
+    _SESSIONS[key] = (sess, vehicle, route, spat)
+    return sess
+
+
+def clear_session_cache() -> None:
+    while _SESSIONS:
+        _SESSIONS.popitem()[1][0].close()
+
+
 class EcoDrivingMPC:
     """Receding-horizon controller with fit / control (mpc.py:344-411)."""
 
@@ -340,9 +365,9 @@ class EcoDrivingMPC:
             raise ValueError("horizon must be >= 1")
         self.route_ = route
         self.spat_ = spat
-        self.session_ = MpcSession(self.vehicle, route, spat, gamma=self.gamma, grids=self.grids,
-                                   penalty=self.penalty, horizon=self.horizon, backend=self.backend,
-                                   teleport=self.teleport, use_terminal_field=self.use_terminal_field)
+        self.session_ = _session_for(self.vehicle, route, spat, gamma=self.gamma, grids=self.grids,
+                                     penalty=self.penalty, horizon=self.horizon, backend=self.backend,
+                                     teleport=self.teleport, use_terminal_field=self.use_terminal_field)
         values, self.fit_stats_ = self.session_.fit()
         self.terminal_field_ = (TerminalCostField(values=values, route_name=route.name, gamma=self.gamma,
                                                   grids=self.grids, penalty=self.penalty)
