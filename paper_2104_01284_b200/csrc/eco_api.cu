@@ -154,7 +154,7 @@ struct Geometry {
     DBuf<RowRec<Real>> row;
     DBuf<RowRec2<Real>> row2;
     DBuf<TilePlan> tiles;
-    DBuf<int32_t> order;
+    DBuf<int32_t> order, rank_of;
     int h_gmax[4] = {0, 0, 0, 0};     // max feasible actions of a plane
     int64_t rows_total = 0;
     int tj = 0, nchunk = 0, band_cap = 0;   // stage-kernel tile shape the plans were built for
@@ -209,12 +209,12 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     const size_t ntiles = (size_t)npi * G.nchunk;
     if (G.tiles.n != ntiles) G.tiles.alloc(ntiles);
     if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
+    if (G.order.n != ntiles) { G.order.alloc(ntiles); G.rank_of.alloc(ntiles); }
+    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.tj, g.nx, G.order.p, G.rank_of.p);
+    ECO_CUDA(cudaGetLastError());
     dim3 tgrid(g.nv * G.nchunk, g.P);
     geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
-        G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p);
-    ECO_CUDA(cudaGetLastError());
-    if (G.order.n != ntiles) G.order.alloc(ntiles);
-    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.tj, g.nx, G.order.p);
+        G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
     ECO_CUDA(cudaGetLastError());
     if (launches) *launches += 6;
 }
@@ -309,7 +309,18 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
     if (MODE == 0) {
         auto k = count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>;
         set_smem_attr(k, tc.smem);
-        k<<<grid, block, tc.smem, st>>>(a);
+        // programmatic dependent launch: the prologue overlaps the previous kernel's tail
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(block);
+        lc.dynamicSmemBytes = tc.smem;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = env_int("ECO_PDL", 1) ? 1 : 0;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        ECO_CUDA(cudaLaunchKernelEx(&lc, k, a));
     } else {
         set_smem_attr(field_stage_kernel<Real>, tc.smem);
         field_stage_kernel<Real><<<grid, block, tc.smem, st>>>(a);
@@ -374,6 +385,7 @@ void check_problem(const EcoProblem* pr) {
         throw ArgError{"grid sizes must be n_v,n_soc,n_t >= 2 and n_te,n_tb >= 1"};
     if (pr->n_v >= (1 << 23)) throw ArgError{"n_v too large"};
     if (pr->n_soc > 32767) throw ArgError{"n_soc must be < 32768"};
+    if ((int64_t)pr->n_te * pr->n_tb > 8192) throw ArgError{"n_te * n_tb must be <= 8192"};
     if (!pr->te_axis || !pr->tb_axis || !pr->soc_axis) throw ArgError{"null axis"};
 }
 

@@ -28,6 +28,7 @@ constexpr uint32_t kRecZoff = 0xFFFFu;
 constexpr uint32_t kRecDzh = 1u << 16;     // wz > 0: time blend uses zlo+1 (K:513)
 constexpr uint32_t kRecDvh = 1u << 17;     // ivhi = ivlo + 1
 constexpr uint32_t kRecGated = 1u << 18;   // v_next > 0: arrival gated on green (K:496)
+constexpr int kRecUShift = 19;             // flat action index in bits 19..31 (U <= 8192)
 
 template <typename Real>
 struct alignas(4 * sizeof(Real)) ActRec {  // per feasible action of a source plane
@@ -132,7 +133,7 @@ geom_pairs_kernel(const EcoPlant* __restrict__ plant, const DevPlan* __restrict_
             a.c1 = (Real)c1;
             // zoff saturates at n_t: any larger shift leaves the ladder
             a.meta = (uint32_t)min(zoff, g.nt) | (wz > 0.0 ? kRecDzh : 0u) | (ivhi != ivlo ? kRecDvh : 0u) |
-                     (v2 > 0.0 ? kRecGated : 0u);
+                     (v2 > 0.0 ? kRecGated : 0u) | ((uint32_t)u << kRecUShift);
             out.act[k] = a;
         }
         __syncthreads();
@@ -252,6 +253,10 @@ struct alignas(16) RowRec2 {   // shared-memory row record: band bases of the tw
 // into shared memory.  nseg < 0: footprint exceeds the cap (L1 path).
 constexpr int kMaxSeg = 40;
 struct TilePlan {
+    int32_t iv, j0, tja, count;       // source plane, first SoC row, rows, feasible actions (0: stop skip)
+    int32_t moving;                   // v_src[iv] > 0
+    int32_t pad;
+    int64_t row_off;                  // row records of (plan, iv) start here
     int32_t nseg;
     int32_t band;                     // staged elements
     int32_t gofs[kMaxSeg];            // element offset of (plane, first row, t = 0) within a level
@@ -263,7 +268,8 @@ struct TilePlan {
 template <typename Real>
 __global__ void __launch_bounds__(256)
 geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap, TilePlan* __restrict__ tiles,
-                  RowRec2<Real>* __restrict__ row2) {
+                  RowRec2<Real>* __restrict__ row2, const int32_t* __restrict__ rank_of,
+                  const DevPlan* __restrict__ plans, const double* __restrict__ vaxes) {
     extern __shared__ int32_t s_lohi[];
     int32_t* s_lo = s_lohi;
     int32_t* s_hi = s_lohi + d.nv;
@@ -290,8 +296,16 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
         if (dhi != dlo) { atomicMin(&s_lo[dhi], jl); atomicMax(&s_hi[dhi], jh); }
     }
     __syncthreads();
-    TilePlan* tp = tiles + pi * nchunk + c;
+    const size_t tbase = (size_t)p * d.nv * nchunk;
+    TilePlan* tp = tiles + tbase + rank_of[tbase + (size_t)iv * nchunk + c];
     if (threadIdx.x == 0) {
+        const double v = vaxes[(size_t)p * d.nv + iv];
+        tp->iv = iv;
+        tp->j0 = j0;
+        tp->tja = tja;
+        tp->count = (plans[p].src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : n;   // K:458-459
+        tp->moving = v > 0.0;
+        tp->row_off = g.row_off[pi];
         int ns = 0, run = 0, ok = d.nv <= 1024;
         for (int q = 0; q < d.nv && ok; ++q) {
             s_segof[q] = -1;
@@ -335,7 +349,7 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
 
 // per plan: tiles sorted by descending work (count * rows), ties by index
 __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int tj, int nx,
-                                  int32_t* __restrict__ order) {
+                                  int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
     const int p = blockIdx.x;
     const int nt_ = nv * nchunk;
     const int32_t* c = count + (size_t)p * nv;
@@ -349,6 +363,7 @@ __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int
             rank += (wj > w) || (wj == w && j < i);
         }
         order[(size_t)p * nt_ + rank] = i;
+        rank_of[(size_t)p * nt_ + i] = rank;
     }
 }
 
@@ -439,6 +454,11 @@ __device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream
+// start its J-independent prologue during this kernel's tail, and wait for
+// the previous kernel's results only where the cost-to-go is first read.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -481,19 +501,19 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
     if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
-    // tiles are visited heaviest first (tile_order)
-    const int tile = a.order ? a.order[rank] : rank;
-    const int iv = tile / a.nchunk;
-    const int chunk = tile - iv * a.nchunk;
-    const int j0 = chunk * a.tj;
+    // tiles are visited heaviest first: tiles[] is stored in that order and
+    // carries everything the prologue needs (one round trip)
+    const TilePlan* tp = a.tiles + rank;
+    const int iv = tp->iv;
+    const int j0 = tp->j0;
+    const int tja = tp->tja;
+    const int count = tp->count;
     const int nt = a.nt, nx = a.nx;
-    const int tja = min(a.tj, nx - j0);
     const int plane = nx * nt;
     const int tstates = tja * nt;
-    const double v = a.v_src[iv];
-    const int count = (a.src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : a.count[iv];   // K:458-459
     const size_t obase = (size_t)iv * plane + (size_t)j0 * nt;
     if (count == 0) {
+        pdl_wait();
         for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
             a.J_out[obase + f] = (Real)INFINITY;
             if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
@@ -501,6 +521,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         }
         return;
     }
+    const double v = tp->moving ? 1.0 : 0.0;       // only its sign is used below
     const TileSmem<Real> L(nt, a.tj, a.slices, a.count_max, a.band_cap);
     uint8_t* s_green = smem + L.green;
     Real* s_best = (Real*)(smem + L.red_best);
@@ -510,16 +531,16 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         const uint8_t g = a.green[i];
         s_green[i] = g;
         red |= (g == 0);
-        if (v == 0.0) held |= (a.dep_ok[i] == 0) | (a.wait[i] > 0.0);
+        held |= (a.dep_ok[i] == 0) | (a.wait[i] > 0.0);
     }
     // any red arrival sample at all?  (plain / stop destinations: never)
     const bool any_red = __syncthreads_or(red) != 0;
     // a standstill plane whose node never holds (no red wait, no stop dwell,
     // departures always allowed) moves exactly like a moving one (K:528-533)
-    const bool any_hold = __syncthreads_or(held) != 0;
+    const bool any_hold = __syncthreads_or(held) != 0 && v == 0.0;
 
     const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
-    const RowRec<Real>* rows = a.row + a.row_off[iv] + j0;     // + k * nx + r
+    const RowRec<Real>* rows = a.row + tp->row_off + j0;       // + k * nx + r
     const int S = a.S;
     const int slice = threadIdx.x / S;
     const int tid = threadIdx.x - slice * S;
@@ -527,14 +548,26 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     unsigned long long nlive = 0;
 
     const bool fast = v > 0.0 || !any_hold;
-    const TilePlan* tp = a.tiles ? a.tiles + (size_t)iv * a.nchunk + chunk : nullptr;
-    const int nseg = tp ? tp->nseg : -1;
+    const int nseg = tp->nseg;
     Real* s_band = (Real*)(smem + L.band);
     RowRec2<Real>* s_rr = (RowRec2<Real>*)(smem + L.rr);
     ActRec<Real>* s_act = (ActRec<Real>*)(smem + L.act);
-    if (fast && nseg >= 0 && count <= a.count_max) {
-        // ---- stage with cp.async: the tile's footprint of J_next (precomputed
-        //      segments), its row records and the plane's action records
+    const bool staged = fast && nseg >= 0 && count <= a.count_max;
+    if (staged) {
+        // ---- stage with cp.async: the plane's action records and the tile's
+        //      row records (route geometry), then -- once the previous stage
+        //      has completed -- the tile's footprint of J_next
+        const RowRec2<Real>* rr_src = a.row2 + tp->row_off + j0;
+        constexpr int rr16 = sizeof(RowRec2<Real>) / 16, act16 = sizeof(ActRec<Real>) / 16;
+        for (int i = threadIdx.x; i < count * tja * rr16; i += blockDim.x) {
+            const int e = i / rr16, h = i - e * rr16;
+            const int k = e / tja, r = e - k * tja;
+            cp_async16(reinterpret_cast<char*>(s_rr + k * a.tj + r) + 16 * h,
+                       reinterpret_cast<const char*>(rr_src + (size_t)k * nx + r) + 16 * h);
+        }
+        for (int i = threadIdx.x; i < count * act16; i += blockDim.x)
+            cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
+        pdl_wait();
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
         const bool v16 = ((nt * (int)sizeof(Real)) & 15) == 0;
         for (int sg = warp; sg < nseg; sg += nwarps) {
@@ -551,16 +584,6 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 }
             }
         }
-        const RowRec2<Real>* rr_src = a.row2 + a.row_off[iv] + j0;
-        constexpr int rr16 = sizeof(RowRec2<Real>) / 16, act16 = sizeof(ActRec<Real>) / 16;
-        for (int i = threadIdx.x; i < count * tja * rr16; i += blockDim.x) {
-            const int e = i / rr16, h = i - e * rr16;
-            const int k = e / tja, r = e - k * tja;
-            cp_async16(reinterpret_cast<char*>(s_rr + k * a.tj + r) + 16 * h,
-                       reinterpret_cast<const char*>(rr_src + (size_t)k * nx + r) + 16 * h);
-        }
-        for (int i = threadIdx.x; i < count * act16; i += blockDim.x)
-            cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
         cp_async_wait_all();
         __syncthreads();
         if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
@@ -633,6 +656,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
             }
         }
     } else if (fast && (nt & 1) == 0) {
+        pdl_wait();
         // ---------------- fast path: constant ladder shift (K:508-518, K:528-533)
         using PR = Pair<Real>;
         const int upr = (nt + kZP - 1) / kZP;
@@ -716,6 +740,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
             }
         }
     } else {
+        pdl_wait();
         // ---------------- per-state path (standstill plane, odd n_t)
         const double t0 = a.t0_dev ? a.t0_dev[0] : a.t0;
         for (int f = tid; f < tstates; f += S) {
@@ -791,7 +816,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
-        a.P_out[obase + f] = bk < 0 ? -1 : u[bk];
+        a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
     }
     if (dbg) {
         __syncthreads();
@@ -803,6 +828,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
 template <typename Real, bool COUNT>
 __global__ void __launch_bounds__(512)
 bellman_stage_kernel(StageArgs<Real> a) {
+    pdl_launch_dependents();
     if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
     stage_tile<Real, COUNT>(a, blockIdx.x, smem);

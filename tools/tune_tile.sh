@@ -1,6 +1,7 @@
 #!/bin/bash
 # Per-stage sweep time of the C2 workload for several tile shapes / band caps.
-for cfg in "2 16 32" "4 16 40" "2 8 32"; do
+CFGS=("2 16 40" "4 16 40" "4 8 40" "2 8 40")
+for cfg in "${CFGS[@]}"; do
   set -- $cfg
   ECO_TILE_TJ=$1 ECO_TILE_SLICES=$2 ECO_BAND_KB=$3 python tools/profile_c2.py --steps 20 > /tmp/t.log 2>&1
   python3 - "$1" "$2" "$3" <<'PY'
