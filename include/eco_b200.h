@@ -16,8 +16,9 @@
  *                         (loop of _kernels.field_sweep _kernels.py:801-865)
  *   eco_mpc_run        <- EcoDrivingMPC.fit + simulate_closed_loop
  *                                                  mpc.py:379-391, 513-596
- *   eco_solve_batch    <- run_bench inner loop    bench.py:136-148
- *                         (many independent solve_horizon calls)
+ *   eco_batch_*, eco_solve_batch
+ *                      <- run_bench inner loop    bench.py:136-148
+ *                         (many independent build_context + solve_horizon)
  *
  * Conventions (dp.py:383-384, _kernels.py:540-545): infeasible cost-to-go is
  * exactly j_inf, infeasible policy entries are -1, policy values are flat
@@ -37,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECO_ABI_VERSION 1
+#define ECO_ABI_VERSION 2
 
 #define ECO_MAX_GEARS 16
 #define ECO_MAX_AXIS 32
@@ -245,13 +246,38 @@ int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,
                         double* final_state, int32_t flags, EcoStats* stats);
 int32_t eco_session_destroy(EcoSession* sess);
 
-/* Batch of independent horizon solves sharing one route geometry (C4):
- * scenario i starts at node s[i], time t_start[i] with its own SPaT
- * (routes[i]).  Writes the start-node cost-to-go J0 (n_scen, n_v, n_soc, n_t)
- * and its policy P0 when the pointers are non-NULL. */
-int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* routes,
-                        int32_t n_scen, const int32_t* s, const double* t_start,
-                        const EcoMpcConfig* cfg, double* J0, int32_t* P0,
+/* Phase plan of one signal (SignalTiming route.py:50-86): green windows
+ * [win[i][0], win[i][1]) within a cycle, shifted by offset. */
+typedef struct EcoSignalTiming {
+    double cycle, offset;
+    int32_t nwin, reserved;
+    double win[ECO_MAX_WINDOWS][2];
+} EcoSignalTiming;
+
+/* Batch of independent horizon solves sharing one route geometry (C4, the
+ * inner loop of run_bench bench.py:136-148 over build_context dp.py:255-341 +
+ * solve_horizon dp.py:425-475).  The route supplies the geometry (speed
+ * limits, grades, node kinds); its signal arrays are ignored.  Scenario i
+ * starts at node s[i] and clock t_start[i]; its signals are
+ * timings[i * n_signal_nodes + j] for the j-th signal node of the route (in
+ * node order).  The horizon is cfg->horizon clipped at the route end.
+ * cfg->use_terminal_field selects the offline field (built once per batch
+ * object) or zeros (terminal_field=None).  J0 (n_scen, n_v, n_soc, n_t) f64
+ * and P0 (int32) receive each scenario's start-node level when non-NULL.
+ * create/solve/destroy keep the route geometry resident across solves;
+ * eco_solve_batch is the one-shot form.  flags: ECO_RUN_COUNT_LIVE. */
+typedef struct EcoBatch EcoBatch;
+int32_t eco_batch_create(const EcoPlant* plant, const EcoRoute* route,
+                         const EcoMpcConfig* cfg, EcoBatch** out);
+int32_t eco_batch_solve(EcoBatch* batch, int32_t n_scen,
+                        const EcoSignalTiming* timings, const int32_t* s,
+                        const double* t_start, double* J0, int32_t* P0,
+                        int32_t flags, EcoStats* stats);
+int32_t eco_batch_destroy(EcoBatch* batch);
+int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* route,
+                        const EcoMpcConfig* cfg, int32_t n_scen,
+                        const EcoSignalTiming* timings, const int32_t* s,
+                        const double* t_start, double* J0, int32_t* P0,
                         EcoStats* stats);
 
 #ifdef __cplusplus

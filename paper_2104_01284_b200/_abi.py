@@ -21,6 +21,7 @@ MAX_GEARS = 16
 MAX_AXIS = 32
 MAX_MAP = MAX_AXIS * MAX_AXIS
 MAX_WINDOWS = 8
+ABI_VERSION = 2
 
 OK, ERR_ARG, ERR_CUDA, ERR_NODEV = 0, 1, 2, 3
 FP32, FP64 = 0, 1
@@ -179,6 +180,31 @@ class RoutePack:
             sig_nwin=ptr(self.nwin, C.c_int32), sig_win=ptr(self.win, C.c_double))
 
 
+# EcoSignalTiming as a numpy record (arrays of them are passed as void*)
+SIGNAL_TIMING_DTYPE = np.dtype([("cycle", "<f8"), ("offset", "<f8"), ("nwin", "<i4"), ("reserved", "<i4"),
+                                ("win", "<f8", (MAX_WINDOWS, 2))])
+assert SIGNAL_TIMING_DTYPE.itemsize == 152
+
+
+def signal_timings(route, spats) -> np.ndarray:
+    """(len(spats), n_signal_nodes) EcoSignalTiming records: scenario i's
+    phase plan at each signal node of ``route`` (node order)."""
+    nodes = sorted(route.traffic_lights)
+    out = np.zeros((len(spats), len(nodes)), dtype=SIGNAL_TIMING_DTYPE)
+    for i, spat in enumerate(spats):
+        for j, node in enumerate(nodes):
+            tm = spat.timing(route.traffic_lights[node])
+            if len(tm.green_windows) > MAX_WINDOWS:
+                raise ValueError(f"signal {route.traffic_lights[node]}: more than {MAX_WINDOWS} green windows")
+            rec = out[i, j]
+            rec["cycle"] = tm.cycle
+            rec["offset"] = tm.offset
+            rec["nwin"] = len(tm.green_windows)
+            for w, (a, b) in enumerate(tm.green_windows):
+                rec["win"][w] = (a, b)
+    return out
+
+
 # ------------------------------------------------------------------ loading
 
 LIB_NAME = "_eco_b200.so"
@@ -208,7 +234,10 @@ def _declare(lib):
         "eco_session_fit": (_I, [C.c_void_p, _PD, _PD, P(EcoStats)]),
         "eco_session_run": (_I, [C.c_void_p, _I, _I, _PD, P(EcoTrajRow), _PI, _PI, _PI, _PD, _I, P(EcoStats)]),
         "eco_session_destroy": (_I, [C.c_void_p]),
-        "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), _I, _PI, _PD, P(EcoMpcConfig), _PD, _PI,
+        "eco_batch_create": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), P(C.c_void_p)]),
+        "eco_batch_solve": (_I, [C.c_void_p, _I, C.c_void_p, _PI, _PD, _PD, _PI, _I, P(EcoStats)]),
+        "eco_batch_destroy": (_I, [C.c_void_p]),
+        "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _I, C.c_void_p, _PI, _PD, _PD, _PI,
                                  P(EcoStats)]),
     }
     for name, (res, args) in sig.items():
@@ -230,7 +259,7 @@ def lib():
             _LIB = _declare(C.CDLL(str(path)))
         except OSError as exc:
             raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
-        if _LIB.eco_abi_version() != 1:
+        if _LIB.eco_abi_version() != ABI_VERSION:
             raise NativeLibraryError("ABI version mismatch between eco_b200.h and the Python bindings")
     return _LIB
 

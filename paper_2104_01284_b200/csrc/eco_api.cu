@@ -99,6 +99,18 @@ __global__ void to_internal2_kernel(const double* __restrict__ src, Real* __rest
     }
 }
 
+// copy 0 of `levels` levels `stride` elements apart -> contiguous f64
+template <typename Real>
+__global__ void to_external_strided_kernel(const Real* __restrict__ src, double* __restrict__ dst, size_t n,
+                                           int levels, size_t stride, double j_inf) {
+    const size_t total = n * levels;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t l = i / n, e = i - l * n;
+        const double x = (double)src[l * stride + e];
+        dst[i] = (x < j_inf) ? x : j_inf;
+    }
+}
+
 // copy 0 of `levels` stacked levels -> contiguous f64 (infeasible -> j_inf)
 template <typename Real>
 __global__ void to_external_levels_kernel(const Real* __restrict__ src, double* __restrict__ dst, size_t n,
@@ -1048,6 +1060,208 @@ SessionBase* make_session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConf
     return s;
 }
 
+// ------------------------------------------------------------- batches
+// Many independent horizon solves over one route geometry (C4).  The
+// route-level geometry (and the optional terminal field) is built once on the
+// first solve and stays resident; each solve uploads the scenarios' start
+// nodes, clocks and signal timings, builds their ladders and terminal levels
+// on the device, and runs H launches, each sweeping stage k of every scenario
+// of the chunk (bellman_batch_kernel).
+struct BatchBase {
+    int precision = 0;
+    virtual ~BatchBase() = default;
+    virtual void solve(int n_scen, const EcoSignalTiming* tim, const int32_t* s, const double* t_start, double* J0,
+                       int32_t* P0, int flags, EcoStats* stats) = 0;
+};
+
+template <typename Real>
+struct Batch : BatchBase {
+    EcoMpcConfig cfg{};
+    std::vector<double> te_h, tb_h;
+    std::vector<int8_t> kinds;
+    int n = 0, n_sig = 0;
+    double stop_dwell = 0.0;
+    RouteCtx<Real> ctx;
+    DBuf<double> field;
+    DBuf<Real> field_int;
+    DBuf<int32_t> sig_of_node;
+    bool fitted = false;
+    size_t cap = 0;                       // scenarios the per-chunk buffers hold
+    DBuf<EcoSignalTiming> tim;
+    DBuf<int32_t> s_d, h_d, P0_d;
+    DBuf<double> t_d, tdep, wait, tax, J0_d;
+    DBuf<uint8_t> green, dep;
+    DBuf<Real> J;
+    DBuf<unsigned long long> live;
+    cudaStream_t st = 0;
+
+    Batch(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
+        cfg = *c;
+        te_h.assign(c->te_axis, c->te_axis + c->n_te);
+        tb_h.assign(c->tb_axis, c->tb_axis + c->n_tb);
+        cfg.te_axis = te_h.data();
+        cfg.tb_axis = tb_h.data();
+        n = r->node_count;
+        kinds.assign(r->kinds, r->kinds + n);
+        stop_dwell = r->stop_dwell;
+        ctx.init(p, r, &cfg, st);
+        std::vector<int32_t> so(n, -1);
+        for (int m = 0; m < n; ++m)
+            if (kinds[m] == ECO_NODE_SIGNAL) so[m] = n_sig++;
+        sig_of_node.alloc(n);
+        sig_of_node.upload(so.data(), n, st);
+        if (cfg.use_terminal_field) {
+            field.alloc((size_t)n * cfg.n_v * cfg.n_soc);
+            field_int.alloc((size_t)n * cfg.n_v * cfg.n_soc);
+        }
+        live.alloc(1);
+        ECO_CUDA(cudaStreamSynchronize(st));
+        ECO_CUDA(cudaStreamCreate(&st));
+    }
+    ~Batch() override {
+        if (st) cudaStreamDestroy(st);
+    }
+
+    void reserve(size_t B, int H, size_t ns) {
+        if (B <= cap) return;
+        const int nt = cfg.n_t;
+        tim.alloc(B * std::max(1, n_sig));
+        s_d.alloc(B); h_d.alloc(B); t_d.alloc(B);
+        green.alloc(B * (H + 1) * nt); dep.alloc(B * (H + 1) * nt);
+        tdep.alloc(B * (H + 1) * nt); wait.alloc(B * (H + 1) * nt); tax.alloc(B * nt);
+        J.alloc(B * 2 * level_stride(ns));
+        cap = B;
+    }
+
+    void solve(int n_scen, const EcoSignalTiming* tim_h, const int32_t* s_h, const double* t_h, double* J0,
+               int32_t* P0, int flags, EcoStats* stats) override {
+        const int nv = cfg.n_v, nx = cfg.n_soc, nt = cfg.n_t, H = cfg.horizon;
+        const int U = cfg.n_te * cfg.n_tb;
+        const size_t ns = (size_t)nv * nx * nt;
+        const bool count = flags & kRunCountLive;
+        for (int i = 0; i < n_scen; ++i) {
+            if (s_h[i] < 0 || s_h[i] > n - 2) throw ArgError{"scenario start node out of range"};
+            if (!std::isfinite(t_h[i])) throw ArgError{"scenario start time must be finite"};
+        }
+        if (n_sig && n_scen && !tim_h) throw ArgError{"null signal timings"};
+        for (int i = 0; i < n_scen * n_sig; ++i)
+            if (tim_h[i].nwin < 0 || tim_h[i].nwin > ECO_MAX_WINDOWS || !(tim_h[i].cycle > 0.0))
+                throw ArgError{"invalid signal timing"};
+        int64_t launches = 0;
+        double fit_ms = 0.0, sweep_ms = 0.0, all_ms = 0.0;
+        if (!fitted) {
+            EventTimer ft;
+            ft.start(st);
+            ctx.geometry(st, &launches);
+            if (cfg.use_terminal_field) {
+                double fs = 0.0;
+                field_build_impl<Real>(kinds.data(), n, stop_dwell, &cfg, ctx.G, ctx.R, ctx.soc.p, field_int, field,
+                                       st, &launches, &fs);
+            }
+            ft.stop(st);
+            fit_ms = ft.ms();
+            fitted = true;
+        }
+        const int chunk = std::max(1, std::min(env_int("ECO_BATCH_CHUNK", 4096), 65535));
+        const TileCfg tc = tile_cfg(ctx.G, nt, 0);
+        const size_t LV = level_stride(ns), LC = level_copy(ns);
+        LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
+                   cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
+        auto kern = count ? bellman_batch_kernel<Real, true> : bellman_batch_kernel<Real, false>;
+        set_smem_attr(kern, tc.smem);
+        int64_t stages = 0;
+        unsigned long long nlive = 0;
+        if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
+        for (int c0 = 0; c0 < n_scen; c0 += chunk) {
+            const int B = std::min(chunk, n_scen - c0);
+            reserve((size_t)std::min(chunk, n_scen), H, ns);
+            std::vector<int32_t> hh(B);
+            int Hmax = 0;
+            for (int i = 0; i < B; ++i) {
+                const int s = s_h[c0 + i];
+                hh[i] = H < n - 1 - s ? H : n - 1 - s;
+                Hmax = std::max(Hmax, hh[i]);
+                stages += hh[i];
+            }
+            EventTimer all, sw;
+            all.start(st);
+            s_d.upload(s_h + c0, B, st);
+            t_d.upload(t_h + c0, B, st);
+            h_d.upload(hh.data(), B, st);
+            if (n_sig) tim.upload(tim_h + (size_t)c0 * n_sig, (size_t)B * n_sig, st);
+            const unsigned pblocks = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (ns + 255) / 256));
+            batch_prepare_kernel<Real><<<dim3(pblocks, B), 256, 0, st>>>(
+                ctx.R.view, lc, sig_of_node.p, n_sig, tim.p, s_d.p, h_d.p, t_d.p, Hmax,
+                cfg.use_terminal_field ? field.p : nullptr, green.p, dep.p, tdep.p, wait.p, tax.p, J.p, LV, LC);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
+            BatchArgs<Real> ba{};
+            ba.base = stage_args(ctx.G, 0, nullptr, nt, tc);
+            ba.base.live = count ? live.p : nullptr;
+            ba.base.dtg = cfg.dt;
+            ba.base.j_inf = (Real)cfg.j_inf;
+            ba.pair_stride = (size_t)nv * U;
+            ba.tile_stride = nv * tc.nchunk;
+            ba.Hmax = Hmax;
+            ba.s = s_d.p; ba.h = h_d.p;
+            ba.green = green.p; ba.dep_ok = dep.p; ba.t_dep = tdep.p; ba.wait = wait.p; ba.t_axis = tax.p;
+            ba.J = J.p; ba.LV = LV; ba.LC = LC;
+            if (P0 && P0_d.n < (size_t)B * ns) P0_d.alloc((size_t)std::min(chunk, n_scen) * ns);
+            ba.P0 = P0 ? P0_d.p : nullptr;
+            sw.start(st);
+            for (int k = Hmax - 1; k >= 0; --k) {
+                ba.k = k;
+                cudaLaunchConfig_t cl{};
+                cl.gridDim = dim3((unsigned)(nv * tc.nchunk), (unsigned)B);
+                cl.blockDim = dim3((unsigned)(tc.S * tc.slices));
+                cl.dynamicSmemBytes = tc.smem;
+                cl.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = env_int("ECO_PDL", 1) ? 1 : 0;
+                cl.attrs = attr;
+                cl.numAttrs = 1;
+                ECO_CUDA(cudaLaunchKernelEx(&cl, kern, ba));
+                ++launches;
+            }
+            sw.stop(st);
+            if (J0) {
+                if (J0_d.n < (size_t)B * ns) J0_d.alloc((size_t)std::min(chunk, n_scen) * ns);
+                to_external_strided_kernel<Real><<<grid_for((size_t)B * ns), 256, 0, st>>>(J.p, J0_d.p, ns, B, 2 * LV,
+                                                                                          cfg.j_inf);
+                ECO_CUDA(cudaGetLastError());
+                ++launches;
+            }
+            all.stop(st);
+            if (J0) J0_d.download(J0 + (size_t)c0 * ns, (size_t)B * ns, st);
+            if (P0) P0_d.download(P0 + (size_t)c0 * ns, (size_t)B * ns, st);
+            ECO_CUDA(cudaStreamSynchronize(st));
+            sweep_ms += sw.ms();
+            all_ms += all.ms();
+        }
+        if (count) {
+            ECO_CUDA(cudaMemcpyAsync(&nlive, live.p, sizeof nlive, cudaMemcpyDeviceToHost, st));
+            ECO_CUDA(cudaStreamSynchronize(st));
+        }
+        if (stats) {
+            stats->device_ms = all_ms + fit_ms;
+            stats->dominant_ms = sweep_ms;
+            stats->dense_updates = stages * (int64_t)ns * U;
+            stats->live_updates = count ? (int64_t)nlive : -1;
+            stats->stages = stages;
+            stats->kernel_launches = launches;
+        }
+    }
+};
+
+BatchBase* make_batch(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
+    BatchBase* b;
+    if (c->precision == ECO_FP64) b = new Batch<double>(p, r, c);
+    else b = new Batch<float>(p, r, c);
+    b->precision = c->precision;
+    return b;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -1171,10 +1385,42 @@ int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route, const EcoMpcCo
     });
 }
 
-int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* routes, int32_t n_scen, const int32_t* s,
-                        const double* t_start, const EcoMpcConfig* cfg, double* J0, int32_t* P0, EcoStats* stats) {
-    g_err = "eco_solve_batch: not built yet";
-    return ECO_ERR_ARG;
+int32_t eco_batch_create(const EcoPlant* plant, const EcoRoute* route, const EcoMpcConfig* cfg, EcoBatch** out) {
+    return run_guarded([&] {
+        check_plant(plant);
+        check_cfg(cfg);
+        if (!route || !out) throw ArgError{"null pointer argument"};
+        *out = reinterpret_cast<EcoBatch*>(make_batch(plant, route, cfg));
+    });
+}
+
+int32_t eco_batch_solve(EcoBatch* batch, int32_t n_scen, const EcoSignalTiming* timings, const int32_t* s,
+                        const double* t_start, double* J0, int32_t* P0, int32_t flags, EcoStats* stats) {
+    return run_guarded([&] {
+        if (!batch) throw ArgError{"null batch"};
+        if (n_scen < 0) throw ArgError{"n_scen must be >= 0"};
+        if (n_scen > 0 && (!s || !t_start)) throw ArgError{"null pointer argument"};
+        reinterpret_cast<BatchBase*>(batch)->solve(n_scen, timings, s, t_start, J0, P0, flags, stats);
+    });
+}
+
+int32_t eco_batch_destroy(EcoBatch* batch) {
+    delete reinterpret_cast<BatchBase*>(batch);
+    return ECO_OK;
+}
+
+int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* route, const EcoMpcConfig* cfg, int32_t n_scen,
+                        const EcoSignalTiming* timings, const int32_t* s, const double* t_start, double* J0,
+                        int32_t* P0, EcoStats* stats) {
+    return run_guarded([&] {
+        check_plant(plant);
+        check_cfg(cfg);
+        if (!route) throw ArgError{"null pointer argument"};
+        if (n_scen < 0) throw ArgError{"n_scen must be >= 0"};
+        if (n_scen > 0 && (!s || !t_start)) throw ArgError{"null pointer argument"};
+        std::unique_ptr<BatchBase> b(make_batch(plant, route, cfg));
+        b->solve(n_scen, timings, s, t_start, J0, P0, 0, stats);
+    });
 }
 
 }  // extern "C"

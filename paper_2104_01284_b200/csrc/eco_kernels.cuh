@@ -347,24 +347,28 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
     }
 }
 
-// per plan: tiles sorted by descending work (count * rows), ties by index
+// per plan: tiles heaviest first -- planes by descending feasible-action
+// count (ties by plane index), the SoC chunks of a plane consecutively.  The
+// order only balances the load; results do not depend on it.
 __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int tj, int nx,
                                   int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
     const int p = blockIdx.x;
-    const int nt_ = nv * nchunk;
     const int32_t* c = count + (size_t)p * nv;
-    for (int i = threadIdx.x; i < nt_; i += blockDim.x) {
-        const int iv = i / nchunk, ch = i - iv * nchunk;
-        const long w = (long)c[iv] * min(tj, nx - ch * tj);
-        int rank = 0;
-        for (int j = 0; j < nt_; ++j) {
-            const int jv = j / nchunk, jch = j - jv * nchunk;
-            const long wj = (long)c[jv] * min(tj, nx - jch * tj);
-            rank += (wj > w) || (wj == w && j < i);
+    const size_t base = (size_t)p * nv * nchunk;
+    for (int iv = threadIdx.x; iv < nv; iv += blockDim.x) {
+        const int w = c[iv];
+        int r = 0;
+        for (int j = 0; j < nv; ++j) {
+            const int wj = c[j];
+            r += (wj > w) || (wj == w && j < iv);
         }
-        order[(size_t)p * nt_ + rank] = i;
-        rank_of[(size_t)p * nt_ + i] = rank;
+        for (int ch = 0; ch < nchunk; ++ch) {
+            const int rank = r * nchunk + ch;
+            order[base + rank] = iv * nchunk + ch;
+            rank_of[base + iv * nchunk + ch] = rank;
+        }
     }
+    (void)tj; (void)nx;
 }
 
 // ---------------------------------------------------------- stage sweep
@@ -517,7 +521,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
             a.J_out[obase + f] = (Real)INFINITY;
             if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
-            a.P_out[obase + f] = -1;
+            if (a.P_out) a.P_out[obase + f] = -1;
         }
         return;
     }
@@ -816,7 +820,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
-        a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
+        if (a.P_out) a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
     }
     if (dbg) {
         __syncthreads();
@@ -831,6 +835,59 @@ bellman_stage_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
+    stage_tile<Real, COUNT>(a, blockIdx.x, smem);
+}
+
+// Batch of independent solves sharing one route's geometry (run_bench's
+// loop bench.py:136-148, C4): launch k runs stage k of every scenario;
+// blockIdx.y = scenario b, whose plan is s_b + k.  Scenarios whose horizon
+// (clipped at the route end, dp.py:280-281) is <= k have nothing to do.  The
+// cost-to-go ping-pongs between two levels per scenario (level k in buffer
+// k & 1); only stage 0 writes the policy.
+template <typename Real>
+struct BatchArgs {
+    StageArgs<Real> base;         // plan-0 geometry pointers, dims, tile shape, scalars
+    size_t pair_stride;           // nv * U
+    int tile_stride;              // nv * nchunk
+    int k, Hmax;
+    const int32_t* s;             // [B] start node
+    const int32_t* h;             // [B] horizon of the scenario
+    const uint8_t* green;         // [B][Hmax+1][nt]
+    const uint8_t* dep_ok;
+    const double* t_dep;
+    const double* wait;
+    const double* t_axis;         // [B][nt]
+    Real* J;                      // [B][2] levels of LV elements (copy 0 at +0, copy 1 at +LC)
+    size_t LV, LC;
+    int32_t* P0;                  // [B][nv*nx*nt] or nullptr
+};
+
+template <typename Real, bool COUNT>
+__global__ void __launch_bounds__(512)
+bellman_batch_kernel(BatchArgs<Real> ba) {
+    pdl_launch_dependents();
+    const int b = blockIdx.y, k = ba.k;
+    if (k >= ba.h[b]) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    StageArgs<Real> a = ba.base;
+    const size_t p = (size_t)(ba.s[b] + k);
+    a.u += p * ba.pair_stride;
+    a.dt += p * ba.pair_stride;
+    a.c1d += p * ba.pair_stride;
+    a.act += p * ba.pair_stride;
+    a.tiles += p * ba.tile_stride;
+    const size_t lad = (size_t)b * (ba.Hmax + 1);
+    a.green = ba.green + (lad + k + 1) * a.nt;
+    a.dep_ok = ba.dep_ok + (lad + k) * a.nt;
+    a.t_dep = ba.t_dep + (lad + k) * a.nt;
+    a.wait = ba.wait + (lad + k) * a.nt;
+    a.t0_dev = ba.t_axis + (size_t)b * a.nt;
+    Real* Jb = ba.J + (size_t)b * 2 * ba.LV;
+    a.J_next = Jb + ((k + 1) & 1) * ba.LV;
+    a.J_next1 = a.J_next + ba.LC;
+    a.J_out = Jb + (k & 1) * ba.LV;
+    a.J_out1 = a.J_out + ba.LC;
+    a.P_out = (k == 0 && ba.P0) ? ba.P0 + (size_t)b * a.nv * a.nx * a.nt : nullptr;
     stage_tile<Real, COUNT>(a, blockIdx.x, smem);
 }
 

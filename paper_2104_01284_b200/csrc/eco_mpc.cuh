@@ -54,19 +54,18 @@ struct LoopCfg {
     const double* vaxes;        // [n][nv] node speed axes
 };
 
-// _node_time_arrays dp.py:217-252 for one node on the ladder
-__device__ __forceinline__ void node_ladder(const DevRoute& r, int node, const double* t_axis, int nt, int teleport,
-                                            uint8_t* green, uint8_t* dep, double* tdep, double* wait, int z) {
-    const double tz = t_axis[z];
+// _node_time_arrays dp.py:217-252 for one node on the ladder; the signal
+// phase plan (cycle, offset, green windows) is passed explicitly
+__device__ __forceinline__ void ladder_entry(int kind, double cycle, double offset, const double* win, int nwin,
+                                             double dwell, double tz, int teleport, uint8_t* green, uint8_t* dep,
+                                             double* tdep, double* wait, int z) {
     uint8_t g = 1, d = 1;
     double td = tz, w = 0.0;
-    const int kind = r.kinds[node];
     if (kind == ECO_NODE_SIGNAL) {
-        const double* win = r.sig_win + (size_t)node * ECO_MAX_WINDOWS * 2;
-        if (!sig_is_green(r.sig_cycle[node], r.sig_offset[node], win, r.sig_nwin[node], tz)) {
+        if (!sig_is_green(cycle, offset, win, nwin, tz)) {
             g = 0;
             if (teleport) {
-                const double ng = sig_next_green(r.sig_cycle[node], r.sig_offset[node], win, r.sig_nwin[node], tz);
+                const double ng = sig_next_green(cycle, offset, win, nwin, tz);
                 td = ng;
                 w = ng - tz;
             } else {
@@ -74,10 +73,18 @@ __device__ __forceinline__ void node_ladder(const DevRoute& r, int node, const d
             }
         }
     } else if (kind == ECO_NODE_STOP) {
-        td = tz + r.stop_dwell;
-        w = r.stop_dwell;
+        td = tz + dwell;
+        w = dwell;
     }
     green[z] = g; dep[z] = d; tdep[z] = td; wait[z] = w;
+}
+
+__device__ __forceinline__ void node_ladder(const DevRoute& r, int node, const double* t_axis, int nt, int teleport,
+                                            uint8_t* green, uint8_t* dep, double* tdep, double* wait, int z) {
+    (void)nt;
+    ladder_entry(r.kinds[node], r.sig_cycle[node], r.sig_offset[node],
+                 r.sig_win + (size_t)node * ECO_MAX_WINDOWS * 2, r.sig_nwin[node], r.stop_dwell, t_axis[z], teleport,
+                 green, dep, tdep, wait, z);
 }
 
 // terminal seed dp.py:322-334: min(base + w*(xi - xi*)^2, j_inf), j_inf where
@@ -310,6 +317,59 @@ mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, Loo
     rows[st->n_rows] = row;
     st->n_rows += 1;
     st->x[0] = nx0; st->x[1] = nx1; st->x[2] = nx2;
+}
+
+// Batch scenarios (C4): per scenario b the time ladder at t_start[b]
+// (GridSpec.t_axis dp.py:75-77), the node ladders of nodes s_b..s_b+h_b with
+// the scenario's own signal timings, and the terminal level J_{h_b} in buffer
+// h_b & 1 (dp.py:322-334).  grid (blocks, B).
+template <typename Real>
+__global__ void batch_prepare_kernel(DevRoute r, LoopCfg c, const int32_t* __restrict__ sig_of_node, int n_sig,
+                                     const EcoSignalTiming* __restrict__ timings, const int32_t* __restrict__ s_arr,
+                                     const int32_t* __restrict__ h_arr, const double* __restrict__ t_start, int Hmax,
+                                     const double* __restrict__ field, uint8_t* green, uint8_t* dep, double* tdep,
+                                     double* wait, double* t_axis, Real* J, size_t LV, size_t LC) {
+    const int b = blockIdx.y;
+    const int s = s_arr[b], h = h_arr[b];
+    const int nt = c.nt;
+    const double t0 = c.dt * floor(t_start[b] / c.dt);
+    double* tax = t_axis + (size_t)b * nt;
+    const size_t lad = (size_t)b * (Hmax + 1) * nt;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (h + 1) * nt; i += gridDim.x * blockDim.x) {
+        const int k = i / nt, z = i - k * nt;
+        const int node = s + k;
+        const double tz = t0 + c.dt * (double)z;
+        if (k == 0) tax[z] = tz;
+        const int si = sig_of_node[node];
+        const EcoSignalTiming* tm = si >= 0 ? timings + (size_t)b * n_sig + si : nullptr;
+        ladder_entry(r.kinds[node], tm ? tm->cycle : 1.0, tm ? tm->offset : 0.0, tm ? &tm->win[0][0] : nullptr,
+                     tm ? tm->nwin : 0, r.stop_dwell, tz, c.teleport, green + lad, dep + lad, tdep + lad,
+                     wait + lad, i);
+    }
+    const int ncell = c.nv * c.nx;
+    const int total = ncell * nt;
+    Real* Jh = J + (size_t)b * 2 * LV + (h & 1) * LV;
+    Real* Jh1 = Jh + LC;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int cell = i / nt;
+        const int jx = cell - (cell / c.nx) * c.nx;
+        const double base = (c.use_field && field) ? field[(size_t)(s + h) * ncell + cell] : 0.0;
+        const Real val = terminal_value<Real>(base, c.soc_axis[jx], c.soc_target, c.soc_weight, c.j_inf);
+        Jh[i] = val;
+        if (i > 0) Jh1[i - 1] = val;
+    }
+    if (blockIdx.x == 0) {
+        // pads of both buffers (the other buffer's are written here too: the
+        // stage kernel never writes past the level)
+        for (int q = 0; q < 2; ++q) {
+            Real* L0 = J + (size_t)b * 2 * LV + q * LV;
+            Real* L1 = L0 + LC;
+            for (int i = total - 1 + threadIdx.x; i < total + 8; i += blockDim.x) {
+                L1[i] = (Real)INFINITY;
+                if (i >= total) L0[i] = (Real)INFINITY;
+            }
+        }
+    }
 }
 
 }  // namespace eco

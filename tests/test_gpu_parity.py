@@ -300,3 +300,110 @@ def test_closed_loop_urban_c2_fp32_within_0p1pct(vehicle, urban_route):
     assert traj.status == "ok" and traj.n_steps == ref["n_steps"]
     assert abs(traj.fuel_g - ref["fuel_g"]) <= 1e-3 * ref["fuel_g"], (traj.fuel_g, ref["fuel_g"])
     assert abs(traj.travel_time_s - ref["travel_time_s"]) <= 1e-3 * ref["travel_time_s"]
+
+
+# ------------------------------------------------------------ C3 fine grid
+
+C3_GRID = GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2)
+
+
+@pytest.fixture(scope="module")
+def c3_short_ctx(vehicle, urban_route):
+    route, spat = urban_route
+    return build_context(vehicle, route, spat, 60, 30.0, grids=C3_GRID, penalty=PEN, gamma=0.5, horizon=2)
+
+
+def test_c3_fine_grid_fp64_bitwise_vs_oracle(c3_short_ctx):
+    """C3 (350 x 260 x 400, dt = 0.2): two stages against the OpenMP oracle."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    J, P, _ = solve_stacks(c3_short_ctx, "b200-fp64")
+    Jo, Po = O.solve_context(c3_short_ctx, parallel=True)
+    for k in range(2):
+        assert np.array_equal(J[k], Jo[k]), k
+        assert np.array_equal(P[k], Po[k]), k
+
+
+def test_c3_fine_grid_fp32_tolerance_full_horizon(vehicle, urban_route):
+    """C3 at the full H = 20: the fp32 production build against the fp64
+    build (bitwise to the oracle above) at every level."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    route, spat = urban_route
+    ctx = build_context(vehicle, route, spat, 60, 30.0, grids=C3_GRID, penalty=PEN, gamma=0.5, horizon=20)
+    J64, P64, _ = solve_stacks(ctx, "b200-fp64")
+    J32, P32, st = solve_stacks(ctx, "b200", count_live=True)
+    assert st["stages"] == 20 and st["live_updates"] > 0
+    for k in range(20):
+        mask, p999, mx, pol = fp32_agreement(J32[k], P32[k], J64[k], P64[k])
+        assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (k, mask, p999, mx, pol)
+
+
+# ------------------------------------------------------------- C4 batch
+
+def _c4_scenarios(n, H=20):
+    from paper_2104_01284_b200.fixtures import bench_schedule, make_route_urban
+    from paper_2104_01284_b200.route import load_route
+    routes = [load_route(make_route_urban(seed=i)) for i in range(n)]
+    sched = [bench_schedule(r, H, 1, seed=i)[0] for i, (r, _) in enumerate(routes)]
+    return routes, sched
+
+
+def test_c4_batch_fp64_digests(vehicle):
+    """The four golden C4 scenarios (reference solve_horizon digests) in one batch."""
+    from paper_2104_01284_b200.batch import solve_batch
+    cases = golden_json("c4_batch_digests.json")
+    routes, sched = _c4_scenarios(len(cases))
+    assert [(c["s"], c["t_start"]) for c in cases] == sched
+    res = solve_batch(vehicle, routes[0][0], [sp for _, sp in routes], sched, grids=GridSpec(), penalty=PEN,
+                      gamma=0.5, horizon=20, backend="b200-fp64")
+    for i, case in enumerate(cases):
+        assert table_digest(res.J0[i]) == case["J0"], i
+        assert table_digest(res.P0[i]) == case["P0"], i
+
+
+def test_c4_batch_matches_single_solves(vehicle):
+    """fp32 batch == fp32 solve_horizon per scenario, bitwise (same geometry,
+    same tiles), incl. horizons clipped at the route end and repeated solves."""
+    from paper_2104_01284_b200.batch import BatchSolver
+    routes, sched = _c4_scenarios(12)
+    sched[3] = (690, 17.25)        # h = 9
+    sched[7] = (698, 3.5)          # h = 1
+    spats = [sp for _, sp in routes]
+    with BatchSolver(vehicle, routes[0][0], grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20) as bs:
+        res = bs.solve(spats, sched, count_live=True)
+        res2 = bs.solve(spats[::-1], sched[::-1])
+    assert list(res.horizons) == [20] * 3 + [9] + [20] * 3 + [1] + [20] * 4
+    assert res.stats["live_updates"] > 0
+    for i, ((route, spat), (s, t)) in enumerate(zip(routes, sched)):
+        ctx = build_context(vehicle, route, spat, s, t, grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20)
+        r = solve_horizon(ctx, backend="b200")
+        assert np.array_equal(res.J0[i], r.tables[0].values), i
+        assert np.array_equal(res.P0[i], r.policies[0].values), i
+        assert np.array_equal(res2.J0[len(sched) - 1 - i], res.J0[i]), i
+
+
+def test_c4_batch_fp32_tolerance(vehicle):
+    from paper_2104_01284_b200.batch import BatchSolver
+    routes, sched = _c4_scenarios(64)
+    spats = [sp for _, sp in routes]
+    kw = dict(grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20)
+    with BatchSolver(vehicle, routes[0][0], backend="b200-fp64", **kw) as b64, \
+            BatchSolver(vehicle, routes[0][0], backend="b200", **kw) as b32:
+        r64, r32 = b64.solve(spats, sched), b32.solve(spats, sched)
+    mask, p999, mx, pol = fp32_agreement(r32.J0, r32.P0, r64.J0, r64.P0)
+    assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (mask, p999, mx, pol)
+
+
+def test_c4_batch_terminal_field_and_no_teleport(vehicle):
+    """Options of build_context: the offline terminal field and teleport=False."""
+    from paper_2104_01284_b200.batch import solve_batch
+    routes, sched = _c4_scenarios(3)
+    spats = [sp for _, sp in routes]
+    field = build_terminal_cost(routes[0][0], vehicle, gamma=0.5, grids=GridSpec(), penalty=PEN,
+                                backend="b200-fp64")
+    res = solve_batch(vehicle, routes[0][0], spats, sched, grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20,
+                      teleport=False, terminal_field=True, backend="b200-fp64")
+    for i, ((route, spat), (s, t)) in enumerate(zip(routes, sched)):
+        ctx = build_context(vehicle, route, spat, s, t, grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20,
+                            teleport=False, terminal_field=field.values[s + min(20, route.node_count - 1 - s)])
+        J, P = O.solve_context(ctx, parallel=True)
+        assert np.array_equal(res.J0[i], J[0]) and np.array_equal(res.P0[i], P[0]), i

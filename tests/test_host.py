@@ -28,7 +28,7 @@ def test_header_symbols_exported():
     assert len(names) >= 9
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.eco_abi_version() == 1
+    assert lib.eco_abi_version() == _abi.ABI_VERSION
 
 
 def test_library_targets_sm100a():

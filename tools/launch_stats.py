@@ -9,10 +9,7 @@ for r in rows[1:]:
     if len(r) < len(h) or r[ix["Metric Name"]] != "gpu__time_duration.sum":
         continue
     v = float(r[ix["Metric Value"]])
-    if r[ix["Metric Unit"]] == "nsecond":
-        v /= 1000.0
-    elif r[ix["Metric Unit"]] == "msecond":
-        v *= 1000.0
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[ix["Metric Unit"]], 1.0)
     d[r[ix["Kernel Name"]].split("(")[0][:60]].append(v)
 tot = sum(sum(v) for v in d.values())
 for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
