@@ -22,6 +22,15 @@ max over ranks of the device time.
 `--impl reference`: the reference algorithm's CPU implementation (the pinned
 C restatement in oracle/, all host threads) on a bounded sample of the same
 workload: fit + the first M receding-horizon steps.
+
+Other workloads (`--workload`; the default line is C2):
+  c4  BASELINE configs[3]: 4096 independent urban scenarios (route seed i,
+      bench_schedule(route_i, 20, 1, seed=i)[0]), C2 grid, H = 20, no terminal
+      field; sharded over ranks in contiguous blocks (strong scaling, no
+      inter-GPU communication).  One step = one batch solve of the shard.
+  c3  BASELINE configs[2]: one receding-horizon solve on the fine grid
+      350 x 260 x 400 (dt = 0.2 s), urban s = 60, t = 30, H = 20.  Replicas
+      for N > 1 (the slab-partitioned variant is C5).
 """
 
 from __future__ import annotations
@@ -226,7 +235,7 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     tf = ROOT / "profiles" / "stage_kernel_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(args.precision)
+        traffic = json.loads(tf.read_text()).get(f"c2_{args.precision}")
     launches_per_step = rst["kernel_launches"] + fst["kernel_launches"]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -295,6 +304,8 @@ def cpu_baseline(budget_s: float) -> dict:
 def run_reference(args, rank, world):
     if rank != 0:
         return None
+    if args.workload in ("c3", "c4"):
+        return run_reference_other(args, world)
     budget = args.cpu_seconds
     probe = cpu_sample(3)
     per_step = max(probe["loop_s"] / 3, 1e-3)
@@ -320,6 +331,273 @@ def run_reference(args, rank, world):
     }
 
 
+# ------------------------------------------------------------ C4 / C3
+
+def _dist_init(world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        return dist
+    return None
+
+
+def _max_over_ranks(dist, ms):
+    if dist is None:
+        return ms
+    import torch
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _roofline(args, local_rank, live, sweep_s, kernel):
+    import torch
+    peaks = measured_peaks()
+    props = torch.cuda.get_device_properties(local_rank)
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = fp32_peak_tflops(props.multi_processor_count, sm_max)
+    if args.precision == "fp64":
+        peak /= 2.0
+    achieved = FLOPS_PER_LIVE * live / sweep_s / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "stage_kernel_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(f"{args.workload}_{args.precision}")
+    return {"bound": "fp32", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_source": f"CUDA-core FP32 = 2 x 128 x {props.multi_processor_count} SMs x {sm_max:.0f} MHz"
+                           + (" / 2 for FP64" if args.precision == "fp64" else ""),
+            "algorithmic": f"{FLOPS_PER_LIVE} flop x {live} live gathers / summed sweep time"}
+
+
+def c4_inputs(n):
+    from paper_2104_01284_b200 import GridSpec, PenaltyConfig, make_vehicle
+    from paper_2104_01284_b200 import _abi
+    from paper_2104_01284_b200.fixtures import bench_schedule, make_route_urban
+    from paper_2104_01284_b200.route import load_route
+    routes = [load_route(make_route_urban(seed=i)) for i in range(n)]
+    sched = [bench_schedule(r, 20, 1, seed=i)[0] for i, (r, _) in enumerate(routes)]
+    tim = _abi.signal_timings(routes[0][0], [sp for _, sp in routes])
+    return make_vehicle(), routes, sched, tim, GridSpec(), PenaltyConfig()
+
+
+def run_c4(args, rank, world, local_rank):
+    import torch
+    from paper_2104_01284_b200.batch import BatchSolver, shard
+    dist = _dist_init(world, local_rank)
+    backend = "b200-fp64" if args.precision == "fp64" else "b200"
+    vehicle, routes, sched, tim, grids, pen = c4_inputs(args.scenarios)
+    mine = shard(len(sched), rank, world)
+    my_sched = [sched[i] for i in mine]
+    my_spats = [routes[i][1] for i in mine]
+    my_tim = tim[mine.start:mine.stop]
+    bs = BatchSolver(vehicle, routes[0][0], grids=grids, penalty=pen, gamma=0.5, horizon=20, backend=backend)
+    fit = bs.solve(my_spats, my_sched, return_tables=False, timings=my_tim).stats     # geometry build
+    for _ in range(args.warmup):
+        bs.solve(my_spats, my_sched, return_tables=False, timings=my_tim)
+    live = bs.solve(my_spats, my_sched, return_tables=False, count_live=True, timings=my_tim).stats["live_updates"]
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sweep_ms, dense, launches = 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = bs.solve(my_spats, my_sched, return_tables=False, timings=my_tim).stats
+            sweep_ms += st["dominant_ms"]
+            dense += st["dense_updates"]
+            launches += st["kernel_launches"]
+        e1.record(stream)
+        barrier()
+    t_max = _max_over_ranks(dist, e0.elapsed_time(e1))
+    total_dense = dense * world if dist is None else None
+    if dist is not None:
+        t = torch.tensor([float(dense)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        total_dense = float(t.item())
+    # e2e: public API, host timings in, J0 / P0 of every scenario out
+    bs.solve(my_spats, my_sched, timings=my_tim)
+    barrier()
+    a0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = bs.solve(my_spats, my_sched)
+    barrier()
+    e2e_ms = _max_over_ranks(dist, (time.perf_counter() - a0) * 1e3)
+    bs.close()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    out = {
+        "metric": METRIC, "value": total_dense / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (reference fixture generators: urban route seeds 0..N-1, bench_schedule per seed)",
+        "config": {"workload": f"C4: batch of {args.scenarios} independent urban scenarios (own SPaT phasing, "
+                               "start node and clock each), default grid 35x26x40 x 23x30, H=20, terminal_field=None",
+                   "parallelism": f"scenario shards x{world} (no inter-GPU communication)",
+                   "l2": "per-step working set (2.4 GB of levels + 2 GB geometry) exceeds L2; no flush",
+                   "precision": args.precision},
+        "ms_per_solve": t_max / args.steps / (args.scenarios / world),
+        "geometry_ms": fit["device_ms"] - fit["dominant_ms"],
+        "dense_updates_per_step": total_dense / args.steps, "live_updates_per_step_rank0": live,
+        "gpu_launches": int(launches),
+        "e2e": {"value": total_dense / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
+                "h2d_bytes_per_step": int(res.stats["h2d_bytes"]), "d2h_bytes_per_step": int(res.stats["d2h_bytes"])},
+        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_batch_kernel"),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = c4_cpu_baseline(args.cpu_seconds)
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+def c4_cpu_sample(n_solves, threads=0):
+    from oracle import oracle as O
+    from paper_2104_01284_b200 import build_context
+    vehicle, routes, sched, _, grids, pen = c4_inputs(n_solves)
+    ctxs = [build_context(vehicle, r, sp, s, t, grids=grids, penalty=pen, gamma=0.5, horizon=20)
+            for (r, sp), (s, t) in zip(routes, sched)]
+    threads = threads or O.threads_available()
+    t0 = time.perf_counter()
+    for c in ctxs:
+        O.solve_context(c, parallel=True, threads=threads)
+    sec = time.perf_counter() - t0
+    ups = sum(c.horizon for c in ctxs) * grids.n_v * grids.n_soc * grids.n_t * grids.n_t_eng * grids.n_t_bsg
+    return dict(updates=ups, seconds=sec, solves=n_solves, threads=threads)
+
+
+def c4_cpu_baseline(budget_s):
+    probe = c4_cpu_sample(2)
+    n = int(max(2, min(4096, budget_s / max(probe["seconds"] / 2, 1e-3))))
+    s = c4_cpu_sample(n)
+    return {"value": s["updates"] / s["seconds"], "unit": UNIT, "cores": s["threads"], "kind": "port",
+            "sample": f"first {n} of the C4 scenarios solved one after another (oracle/eco_oracle.c two-stage "
+                      f"sweep, {s['threads']} OpenMP threads)", "seconds": s["seconds"],
+            "ms_per_solve": 1e3 * s["seconds"] / n}
+
+
+def c3_context(H=20):
+    from paper_2104_01284_b200 import (GridSpec, PenaltyConfig, build_context, load_fixture_route, make_vehicle)
+    route, spat = load_fixture_route("urban", seed=0)
+    grids = GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2)
+    return build_context(make_vehicle(), route, spat, 60, 30.0, grids=grids, penalty=PenaltyConfig(), gamma=0.5,
+                         horizon=H)
+
+
+def run_c3(args, rank, world, local_rank):
+    import torch
+    from paper_2104_01284_b200 import solve_horizon
+    from paper_2104_01284_b200.dp import solve_stacks
+    dist = _dist_init(world, local_rank)
+    backend = "b200-fp64" if args.precision == "fp64" else "b200"
+    ctx = c3_context()
+    for _ in range(args.warmup):
+        solve_stacks(ctx, backend)
+    live = solve_stacks(ctx, backend, count_live=True)[2]["live_updates"]
+    dev_ms, sweep_ms, dense, launches = 0.0, 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            st = solve_stacks(ctx, backend)[2]
+            dev_ms += st["device_ms"]
+            sweep_ms += st["dominant_ms"]
+            dense += st["dense_updates"]
+            launches += st["kernel_launches"]
+    t_max = _max_over_ranks(dist, dev_ms)
+    if dist is not None:
+        dist.barrier()
+    a0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = solve_horizon(ctx, backend=backend)
+    e2e_ms = _max_over_ranks(dist, (time.perf_counter() - a0) * 1e3)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    ns = ctx.grids.n_v * ctx.grids.n_soc * ctx.grids.n_t
+    out = {
+        "metric": METRIC, "value": dense * world / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (urban route seed 0)",
+        "config": {"workload": "C3: one receding-horizon solve, fine grid 350x260x400 (dt=0.2) x 23x30, urban "
+                               "s=60 t=30, H=20 (geometry of the 20 steps + 20 stage sweeps per step)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "levels of 291 MB exceed L2; no flush", "precision": args.precision,
+                   "timing": "device time per solve from CUDA events on the solver's stream (sum over steps)"},
+        "ms_per_solve": t_max / args.steps, "sweep_ms_per_solve": sweep_ms / args.steps,
+        "dense_updates_per_step": dense / args.steps, "live_updates_per_step": live,
+        "gpu_launches": int(launches),
+        "e2e": {"value": dense * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
+                "h2d_bytes_per_step": int(ns * 8 + 20 * (4 * 8 * ctx.grids.n_t)),
+                "d2h_bytes_per_step": int(21 * ns * 8 + 20 * ns * 4)},
+        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_stage_kernel"),
+        "clocks": clk.summary(),
+    }
+    del res
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        c = c3_context(H=1)
+        t0 = time.perf_counter()
+        O.solve_context(c, parallel=True)
+        sec = time.perf_counter() - t0
+        ups = ns * ctx.grids.n_t_eng * ctx.grids.n_t_bsg
+        out["cpu_baseline"] = {"value": ups / sec, "unit": UNIT, "cores": O.threads_available(), "kind": "port",
+                               "sample": "one C3 Bellman stage (the last of the horizon) with the oracle's "
+                                         "two-stage sweep on all host threads", "seconds": sec}
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference_other(args, world):
+    """--impl reference for C4 / C3: the oracle on a bounded sample."""
+    from oracle import oracle as O
+    times, ups, sample = [], [], ""
+    if args.workload == "c4":
+        probe = c4_cpu_sample(2)
+        n = int(max(2, min(4096, args.cpu_seconds / max(probe["seconds"] / 2, 1e-3))))
+        for _ in range(args.warmup):
+            c4_cpu_sample(2)
+        for _ in range(args.steps):
+            s = c4_cpu_sample(n)
+            times.append(s["seconds"])
+            ups.append(s["updates"])
+        sample = f"first {n} C4 scenarios per step, solved one after another"
+        workload = f"C4: batch of {args.scenarios} urban scenarios, default grid, H=20 (bounded sample)"
+    else:
+        ctx = c3_context(H=1)
+        ns = ctx.grids.n_v * ctx.grids.n_soc * ctx.grids.n_t
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            O.solve_context(ctx, parallel=True)
+            times.append(time.perf_counter() - t0)
+            ups.append(ns * ctx.grids.n_t_eng * ctx.grids.n_t_bsg)
+        sample = "one C3 Bellman stage per step"
+        workload = "C3: fine grid 350x260x400 x 23x30, urban s=60 t=30 (bounded sample)"
+    value = sum(ups) / sum(times)
+    threads = O.threads_available()
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.workload == "c4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference", "config": {"workload": workload},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample + f" (oracle/eco_oracle.c two-stage sweep, {threads} OpenMP threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,12 +607,18 @@ def main():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2")
+    ap.add_argument("--scenarios", type=int, default=4096, help="C4 batch size (all ranks together)")
     args = ap.parse_args()
     rank, world, local_rank = env_rank()
     if world != args.gpus and world == 1:
         world = 1
     if args.impl == "reference":
         out = run_reference(args, rank, world)
+    elif args.workload == "c4":
+        out = run_c4(args, rank, world, local_rank)
+    elif args.workload == "c3":
+        out = run_c3(args, rank, world, local_rank)
     else:
         out = run_ours(args, rank, world, local_rank)
     if out is not None:

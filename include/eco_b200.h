@@ -182,6 +182,12 @@ int32_t eco_abi_version(void);
 const char* eco_last_error(void);
 int32_t eco_device_count(void);
 
+/* The stateless solvers (eco_bellman_step, eco_solve_horizon) keep their
+ * device buffers in a grow-only workspace so repeated calls on one grid
+ * allocate nothing (not thread-safe: one solving thread per process).
+ * This frees it. */
+int32_t eco_release_workspace(void);
+
 /* One backward Bellman step (backward_step, dp.py:365-404).  J_next, J_out
  * are (n_v, n_soc, n_t) f64, P_out int32.  tables may be NULL (plant path). */
 int32_t eco_bellman_step(const EcoPlant* plant, const EcoProblem* prob,

@@ -221,6 +221,7 @@ def _declare(lib):
         "eco_abi_version": (_I, []),
         "eco_last_error": (C.c_char_p, []),
         "eco_device_count": (_I, []),
+        "eco_release_workspace": (_I, []),
         "eco_bellman_step": (_I, [P(EcoPlant), P(EcoProblem), P(EcoStepPlan), P(EcoStage1Tables),
                                   _PD, _PD, _PI, _I, _I, P(EcoStats)]),
         "eco_solve_horizon": (_I, [P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI, _I, _I,

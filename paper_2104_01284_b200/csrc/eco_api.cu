@@ -41,18 +41,28 @@ struct ArgError {
 template <typename T>
 struct DBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;
     DBuf() = default;
     explicit DBuf(size_t count) { alloc(count); }
     void alloc(size_t count) {
         free();
-        n = count;
+        n = cap = count;
         if (count) ECO_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    // grow-only: keeps the allocation when it is large enough
+    void ensure(size_t count) {
+        if (count > cap || !p) {
+            free();
+            if (count) ECO_CUDA(cudaMalloc(&p, count * sizeof(T)));
+            cap = count;
+        }
+        n = count;
     }
     void free() {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
+        cap = 0;
     }
     ~DBuf() { free(); }
     DBuf(const DBuf&) = delete;
@@ -85,7 +95,9 @@ __global__ void to_external_kernel(const Real* __restrict__ src, double* __restr
 // (v, soc, t) levels are stored twice: copy 0 as-is and copy 1 shifted by one
 // element, so the stage kernel reads any two consecutive time samples with one
 // aligned 64-bit load.  level_stride() is the distance between levels.
-__host__ __device__ inline size_t level_copy(size_t ns) { return (ns + 15) & ~size_t(7); }
+// The pad after each copy (>= 128 elements) absorbs the wide-row path's
+// loads past a row's last live state.
+__host__ __device__ inline size_t level_copy(size_t ns) { return (ns + 135) & ~size_t(7); }
 __host__ __device__ inline size_t level_stride(size_t ns) { return 2 * level_copy(ns); }
 
 template <typename Real>
@@ -155,6 +167,9 @@ inline int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+// long time ladders take the wide-row stage path (ECO_WIDE=0 disables it)
+inline bool wide_rows(int nt) { return nt >= 128 && nt % 2 == 0 && env_int("ECO_WIDE", 1) != 0; }
+
 // --------------------------------------------------------- geometry store
 template <typename Real>
 struct Geometry {
@@ -215,7 +230,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     ECO_CUDA(cudaGetLastError());
     // staging plans of the (v, soc, t) stage kernel's tiles
     const int upr = (g.nt + kZP - 1) / kZP;
-    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", std::max(1, 16 / upr))));
+    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", wide_rows(g.nt) ? 2 : std::max(1, 16 / upr))));
     G.nchunk = (g.nx + G.tj - 1) / G.tj;
     G.band_cap = env_int("ECO_BAND_KB", 40) * 1024 / (int)sizeof(Real);
     const size_t ntiles = (size_t)npi * G.nchunk;
@@ -236,6 +251,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
 struct TileCfg {
     int tj, nchunk, S, slices;
     int count_max = 0, band_cap = 0;
+    int wide = 0;
     size_t smem;
 };
 
@@ -254,6 +270,18 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode) {
     } else {
         t.tj = G.tj;
         t.nchunk = G.nchunk;
+        if (wide_rows(nt)) {
+            // wide rows: S = warps per row x 32 x tj, no shared-memory staging
+            t.wide = (nt + 64 * kMW - 1) / (64 * kMW);
+            t.S = 32 * t.wide * t.tj;
+            if (t.S > 256) throw ArgError{"tile too large for the wide-row path (lower ECO_TILE_TJ)"};
+            t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", std::max(1, 256 / t.S)), 256 / t.S));
+            t.count_max = std::max(1, G.h_gmax[0]);   // record staging, no J band
+            t.band_cap = 0;
+            t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, 0).total;
+            if (t.smem > 227 * 1024) throw ArgError{"tile reduction buffers exceed shared memory"};
+            return t;
+        }
         const int upr = (nt + kZP - 1) / kZP;
         // threads per action slice: one per kZP ladder states of the tile (a
         // warp may hold two slices); the per-state path strides over states
@@ -294,6 +322,7 @@ StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int n
     a.slices = tc.slices;
     a.count_max = tc.count_max;
     a.band_cap = tc.band_cap;
+    a.wide = tc.wide;
     a.gamma = g.gamma;
     return a;
 }
@@ -319,7 +348,8 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
     const unsigned grid = (unsigned)(a.nv * tc.nchunk);
     const unsigned block = (unsigned)(tc.S * tc.slices);
     if (MODE == 0) {
-        auto k = count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>;
+        auto k = tc.wide ? (count ? bellman_wide_kernel<Real, true> : bellman_wide_kernel<Real, false>)
+                         : (count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>);
         set_smem_attr(k, tc.smem);
         // programmatic dependent launch: the prologue overlaps the previous kernel's tail
         cudaLaunchConfig_t lc{};
@@ -438,6 +468,26 @@ struct TablesDev {
 };
 
 // --------------------------------------------------------- horizon solve
+template <typename Real>
+struct HorizonWorkspace {
+    Geometry<Real> G;
+    DBuf<Real> J;
+    DBuf<int32_t> P;
+    DBuf<double> tmp;
+    DBuf<unsigned long long> live;
+    void release() {
+        G.~Geometry<Real>();
+        new (&G) Geometry<Real>();
+        J.free(); P.free(); tmp.free(); live.free();
+    }
+};
+
+template <typename Real>
+HorizonWorkspace<Real>& horizon_workspace() {
+    static HorizonWorkspace<Real> w;
+    return w;
+}
+
 // dp.py:425-475 / dp.py:557-610: H plans, terminal -> J stack, P stack.
 template <typename Real>
 void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H,
@@ -478,20 +528,27 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     d_soc.upload(pr->soc_axis, nx, st);
     TablesDev tdev;   // plant path: no tables
 
-    EventTimer all, sweep;
-    all.start(st);
-    Geometry<Real> G;
+    // device buffers persist across calls (grow-only workspace): repeated
+    // solves of one grid allocate nothing; eco_release_workspace() frees them
+    HorizonWorkspace<Real>& W = horizon_workspace<Real>();
+    Geometry<Real>& G = W.G;
     G.dims = GeomDims{H, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
-    // toy mode: each step has its own table; geometry built per plan below
-    if (!tabs) build_geometry(G, d_plant.p, d_plans.p, d_v.p, d_te.p, d_tb.p, d_soc.p, tdev.view, st, &launches);
-
     const size_t LV = level_stride(ns), LC = level_copy(ns);
-    DBuf<Real> d_J((H + 1) * LV);
-    DBuf<int32_t> d_P((size_t)H * ns);
-    DBuf<double> d_tmp(ns * (H + 1));
-    DBuf<unsigned long long> d_live(1);
+    W.J.ensure((H + 1) * LV);
+    W.P.ensure((size_t)H * ns);
+    W.tmp.ensure(ns * (H + 1));
+    W.live.ensure(1);
+    DBuf<Real>& d_J = W.J;
+    DBuf<int32_t>& d_P = W.P;
+    DBuf<double>& d_tmp = W.tmp;
+    DBuf<unsigned long long>& d_live = W.live;
     ECO_CUDA(cudaMemsetAsync(d_live.p, 0, sizeof(unsigned long long), st));
     d_tmp.upload(terminal, ns, st);
+
+    EventTimer all, sweep;
+    all.start(st);
+    // toy mode: each step has its own table; geometry built per plan below
+    if (!tabs) build_geometry(G, d_plant.p, d_plans.p, d_v.p, d_te.p, d_tb.p, d_soc.p, tdev.view, st, &launches);
     to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(d_tmp.p, d_J.p + (size_t)H * LV, ns, pr->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++launches;
@@ -515,7 +572,8 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     DBuf<int8_t> d_kinds(H);
     d_kinds.upload(hkinds.data(), H, st);
     SolveSync ssync;
-    const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0;
+    const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
+                            !tcs[0].wide;
     sweep.start(st);
     if (persistent) {
         SolveArgs<Real> sa = solve_args(G, tcs[0], nt);
@@ -928,7 +986,7 @@ struct Session : SessionBase {
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
         const TileCfg tc = tile_cfg(ctx.G, nt, 0);
-        const bool persistent = env_int("ECO_PERSISTENT", 0) != 0;
+        const bool persistent = env_int("ECO_PERSISTENT", 0) != 0 && !tc.wide;
         int64_t stages = 0;
         int nev = 0;
         auto enqueue = [&](cudaStream_t qs, bool capturing) {
@@ -1167,6 +1225,7 @@ struct Batch : BatchBase {
         const size_t LV = level_stride(ns), LC = level_copy(ns);
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
+        if (tc.wide) throw ArgError{"batch solves support n_t < 128 (the wide-row path is single-solve only)"};
         auto kern = count ? bellman_batch_kernel<Real, true> : bellman_batch_kernel<Real, false>;
         set_smem_attr(kern, tc.smem);
         int64_t stages = 0;
@@ -1270,6 +1329,13 @@ extern "C" {
 int32_t eco_abi_version(void) { return ECO_ABI_VERSION; }
 
 const char* eco_last_error(void) { return g_err.c_str(); }
+
+int32_t eco_release_workspace(void) {
+    return run_guarded([&] {
+        horizon_workspace<float>().release();
+        horizon_workspace<double>().release();
+    });
+}
 
 int32_t eco_device_count(void) {
     int n = 0;

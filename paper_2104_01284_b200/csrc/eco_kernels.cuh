@@ -406,6 +406,7 @@ struct StageArgs {
     int nv, nx, nt, U;
     int tj, nchunk, S, slices;    // tile: tj SoC rows; S threads per action slice
     int count_max, band_cap;      // staging capacity: actions per plane, band elements
+    int wide;                     // > 0: wide-row path, warps per row (n_t >= 128)
     int src_kind;
     double t0, dtg, gamma, dwell;
     Real j_inf;
@@ -474,6 +475,14 @@ __device__ __forceinline__ unsigned smid() {
     return r;
 }
 
+#ifndef ECO_WIDE_CHUNKS
+#define ECO_WIDE_CHUNKS 4
+#endif
+#ifndef ECO_WIDE_MINB
+#define ECO_WIDE_MINB 3
+#endif
+constexpr int kMW = ECO_WIDE_CHUNKS;   // wide path: 64-state chunks per warp
+
 template <typename Real>
 struct TileSmem {
     size_t green, red_best, red_arg, rr, act, band, total;
@@ -482,7 +491,9 @@ struct TileSmem {
         green = o;    o = align16(o + (size_t)nt);
         red_best = o; o = align16(o + (size_t)slices * tj * nt * sizeof(Real));
         red_arg = o;  o = align16(o + (size_t)slices * tj * nt * sizeof(int32_t));
-        rr = o;       o = align16(o + (size_t)count_max * tj * sizeof(RowRec2<Real>));
+        rr = o;       o = align16(o + (size_t)count_max * tj *
+                                  (sizeof(RowRec2<Real>) > sizeof(RowRec<Real>) ? sizeof(RowRec2<Real>)
+                                                                                 : sizeof(RowRec<Real>)));
         act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
         band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
         total = o;
@@ -500,7 +511,7 @@ struct TileSmem {
 // copies of J_next (as-is / shifted by one) make every corner pair one aligned
 // 64-bit load.  Standstill planes (v == 0: red-wait / dwell relocation,
 // K:519-535) run a per-state loop.
-template <typename Real, bool COUNT>
+template <typename Real, bool COUNT, bool WIDE = false>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
@@ -556,7 +567,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     Real* s_band = (Real*)(smem + L.band);
     RowRec2<Real>* s_rr = (RowRec2<Real>*)(smem + L.rr);
     ActRec<Real>* s_act = (ActRec<Real>*)(smem + L.act);
-    const bool staged = fast && nseg >= 0 && count <= a.count_max;
+    const bool staged = !WIDE && fast && nseg >= 0 && count <= a.count_max;
     if (staged) {
         // ---- stage with cp.async: the plane's action records and the tile's
         //      row records (route geometry), then -- once the previous stage
@@ -659,7 +670,141 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 s_arg[slice * tj_nt + r * nt + z] = bk[i];
             }
         }
-    } else if (fast && (nt & 1) == 0) {
+    } else if (WIDE && fast) {
+        // the tile's row records and the plane's action records go to shared
+        // memory first (route geometry: no dependency on the previous stage),
+        // so skipped actions cost no memory round trip
+        const bool rec_sm = count <= a.count_max;
+        RowRec<Real>* s_ro = reinterpret_cast<RowRec<Real>*>(smem + L.rr);
+        if (rec_sm) {
+            constexpr int ro16 = sizeof(RowRec<Real>) / 16, act16 = sizeof(ActRec<Real>) / 16;
+            for (int i = threadIdx.x; i < count * tja * ro16; i += blockDim.x) {
+                const int e = i / ro16, h = i - e * ro16;
+                const int k = e / tja, rr = e - k * tja;
+                cp_async16(reinterpret_cast<char*>(s_ro + k * a.tj + rr) + 16 * h,
+                           reinterpret_cast<const char*>(rows + (size_t)k * nx + rr) + 16 * h);
+            }
+            for (int i = threadIdx.x; i < count * act16; i += blockDim.x)
+                cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
+            cp_async_wait_all();
+        }
+        pdl_wait();
+        __syncthreads();
+        // ---------------- wide rows (long time ladders, e.g. C3's n_t = 400):
+        // a warp owns 64 * kMW consecutive ladder states of one row, two per
+        // lane per 64-state chunk.  Each corner row of a chunk is one
+        // coalesced 64-bit load per lane (copy 0 or 1 of J_next by the parity
+        // of the row offset: 256 contiguous bytes per warp); the t' + 1 sample
+        // of the blended column comes from the neighbouring lane.  Loads past
+        // the last live state stay inside the level's pad (level_copy).
+        using PR = Pair<Real>;
+        const int lane = threadIdx.x & 31;
+        const int w = tid >> 5;
+        const int r = w / a.wide, seg = w - r * a.wide;
+        const int zs = seg * 64 * kMW;                   // first state of the warp
+        const int zb = zs + 2 * lane;                    // first state of the lane's pair in chunk 0
+        Real best[2 * kMW];
+        int bk[2 * kMW];
+#pragma unroll
+        for (int i = 0; i < 2 * kMW; ++i) { best[i] = a.j_inf; bk[i] = -1; }
+        if (r < tja && zs < nt) {
+            const Real* __restrict__ J0 = a.J_next;
+            const Real* __restrict__ J1 = a.J_next1;
+            const unsigned full = 0xffffffffu;
+            for (int k = slice; k < count; k += a.slices) {
+                const RowRec<Real> ro = rec_sm ? s_ro[k * a.tj + r] : rows[(size_t)k * nx + r];
+                const int zl = ro.zlim;
+                if (zs > zl) continue;                       // warp-uniform; also: SoC move off the hull
+                const ActRec<Real> rc = rec_sm ? s_act[k] : acts[k];
+                const int dv = (rc.meta & kRecDvh) ? plane : 0;
+                const int dx = ro.wx > (Real)0 ? nt : 0;
+                const unsigned off = (unsigned)ro.off;       // (ivlo, jxlo, t' = zoff)
+                const Real* b00 = ((off & 1u) ? J1 : J0) + (off & ~1u) + zb;
+                const Real* b10 = b00 + dv;
+                const Real* b01 = b00 + dx;
+                const Real* b11 = b01 + dv;
+                // chunks holding a live pair or the t' + 1 sample of one (chunk
+                // 0 always does: its unconditional load keeps the four corner
+                // pointers in registers for the others' immediate offsets)
+                const int mlive = min(kMW, ((zl + 1 - zs) >> 6) + 1);
+                PR col[kMW];
+#pragma unroll
+                for (int m = 0; m < kMW; ++m) {
+                    col[m] = PR{(Real)INFINITY, (Real)INFINITY};
+                    if (m == 0 || m < mlive) {
+                        const V2 t00 = __ldg(reinterpret_cast<const V2*>(b00 + 64 * m));
+                        const V2 t10 = __ldg(reinterpret_cast<const V2*>(b10 + 64 * m));
+                        const V2 t01 = __ldg(reinterpret_cast<const V2*>(b01 + 64 * m));
+                        const V2 t11 = __ldg(reinterpret_cast<const V2*>(b11 + 64 * m));
+                        const PR lo = p_lerp(PR{t00.x, t00.y}, PR{t10.x, t10.y}, rc.wv);   // v inside (K:335-337)
+                        const PR hi = p_lerp(PR{t01.x, t01.y}, PR{t11.x, t11.y}, rc.wv);
+                        col[m] = p_lerp(lo, hi, ro.wx);                                  // then soc
+                    }
+                }
+                PR F[kMW];
+                if (rc.meta & kRecDzh) {                     // then t (K:361)
+                    // t' + 2 sample of lane 31's last pair: the first sample
+                    // after the warp's range (same address in every lane)
+                    Real tail = (Real)INFINITY;
+                    if (zl >= zs + 64 * kMW - 1) {
+                        const int q = 64 * kMW - 2 * lane;
+                        const Real lo = lerp(__ldg(b00 + q), __ldg(b10 + q), rc.wv);
+                        const Real hi = lerp(__ldg(b01 + q), __ldg(b11 + q), rc.wv);
+                        tail = lerp(lo, hi, ro.wx);
+                    }
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) {
+                        Real nxt = __shfl_down_sync(full, col[m].x, 1);
+                        const Real first = m + 1 < kMW ? __shfl_sync(full, col[(m + 1) % kMW].x, 0) : tail;
+                        if (lane == 31) nxt = first;
+                        F[m] = p_addc(p_lerp(col[m], PR{col[m].y, nxt}, rc.wz), rc.c1);
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) F[m] = p_addc(col[m], rc.c1);
+                }
+                const int zoff = (int)(rc.meta & kRecZoff);
+                if (any_red && (rc.meta & kRecGated)) {
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) {
+                        const int z = zb + 64 * m;
+                        const bool ok0 = z <= zl && s_green[z + zoff] != 0;       // K:516
+                        const bool ok1 = z + 1 <= zl && s_green[z + 1 + zoff] != 0;
+                        if (COUNT) nlive += ok0 + ok1;
+                        const bool u0 = ok0 && F[m].x < best[2 * m];
+                        const bool u1 = ok1 && F[m].y < best[2 * m + 1];
+                        best[2 * m] = u0 ? F[m].x : best[2 * m];
+                        bk[2 * m] = u0 ? k : bk[2 * m];
+                        best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
+                        bk[2 * m + 1] = u1 ? k : bk[2 * m + 1];
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) {
+                        const int z = zb + 64 * m;
+                        const bool ok0 = z <= zl, ok1 = z < zl;
+                        if (COUNT) nlive += ok0 + ok1;
+                        const bool u0 = (F[m].x < best[2 * m]) & ok0;
+                        const bool u1 = (F[m].y < best[2 * m + 1]) & ok1;
+                        best[2 * m] = u0 ? F[m].x : best[2 * m];
+                        bk[2 * m] = u0 ? k : bk[2 * m];
+                        best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
+                        bk[2 * m + 1] = u1 ? k : bk[2 * m + 1];
+                    }
+                }
+            }
+        }
+        if (r < tja) {
+#pragma unroll
+            for (int i = 0; i < 2 * kMW; ++i) {
+                const int z = zb + 64 * (i >> 1) + (i & 1);
+                if (z < nt) {
+                    s_best[slice * tj_nt + r * nt + z] = best[i];
+                    s_arg[slice * tj_nt + r * nt + z] = bk[i];
+                }
+            }
+        }
+    } else if (!WIDE && fast && (nt & 1) == 0) {
         pdl_wait();
         // ---------------- fast path: constant ladder shift (K:508-518, K:528-533)
         using PR = Pair<Real>;
@@ -836,6 +981,18 @@ bellman_stage_kernel(StageArgs<Real> a) {
     if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
     stage_tile<Real, COUNT>(a, blockIdx.x, smem);
+}
+
+// Wide-row variant (n_t >= 128, StageArgs::wide > 0): blocks of <= 256
+// threads with up to 128 registers, so the four corner pointers and the
+// eight in-flight chunk loads of a warp stay in registers.
+template <typename Real, bool COUNT>
+__global__ void __launch_bounds__(256, ECO_WIDE_MINB)
+bellman_wide_kernel(StageArgs<Real> a) {
+    pdl_launch_dependents();
+    if (a.status && *a.status != 0) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    stage_tile<Real, COUNT, true>(a, blockIdx.x, smem);
 }
 
 // Batch of independent solves sharing one route's geometry (run_bench's

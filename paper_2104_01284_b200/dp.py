@@ -388,6 +388,11 @@ class SolveResult:
         return self.tables[0]
 
 
+def release_workspace():
+    """Free the device workspace the stateless solvers keep between calls."""
+    _abi.check(_abi.lib().eco_release_workspace(), "eco_release_workspace")
+
+
 def solve_stacks(ctx, backend: str = "b200", count_live: bool = False):
     """Device solve of a context -> (J stack (H+1, n_v, n_soc, n_t) f64,
     P stack (H, ...) int32, stats).  ``ctx`` only needs the reference
