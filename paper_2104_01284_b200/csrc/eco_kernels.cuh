@@ -690,6 +690,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         }
         pdl_wait();
         __syncthreads();
+        if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
         // ---------------- wide rows (long time ladders, e.g. C3's n_t = 400):
         // a warp owns 64 * kMW consecutive ladder states of one row, two per
         // lane per 64-state chunk.  Each corner row of a chunk is one

@@ -7,7 +7,12 @@ if len(sys.argv) > 2 and sys.argv[1] == "--parse":
     import collections, statistics as S
     blk = open(sys.argv[2]).read().split("stage k=")[-1]
     rows = [l.split() for l in blk.splitlines() if l.strip().startswith("cta")]
-    st = [float(r[9]) for r in rows]; lp = [float(r[13]) for r in rows]; en = [float(r[15]) for r in rows]
+    st = [float(r[9]) for r in rows]; sg = [float(r[11]) for r in rows]
+    lp = [float(r[13]) for r in rows]; en = [float(r[15]) for r in rows]
+    pro = [b - a for a, b in zip(st, sg) if b > 0]; loop = [c - b for b, c in zip(sg, lp) if b > 0]
+    mrg = [d - c for c, d in zip(lp, en)]
+    if pro:
+        print(f"prologue med {S.median(pro):.1f} | loop med {S.median(loop):.1f} max {max(loop):.1f} | merge med {S.median(mrg):.1f}us")
     path = [int(r[5]) for r in rows]; work = [int(r[7]) for r in rows]
     span = max(en) - min(st)
     print(f"ctas={len(rows)} span={span:.1f}us")
