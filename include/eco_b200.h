@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECO_ABI_VERSION 2
+#define ECO_ABI_VERSION 3
 
 #define ECO_MAX_GEARS 16
 #define ECO_MAX_AXIS 32
@@ -285,6 +285,36 @@ int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* route,
                         const EcoSignalTiming* timings, const int32_t* s,
                         const double* t_start, double* J0, int32_t* P0,
                         EcoStats* stats);
+
+/* Slab-partitioned horizon solve across GPUs (C5; the GPU form
+ * of the reference's v-plane WorkPartition, parallel.py:59-106).  One process
+ * per GPU; rank r of nranks computes the speed planes [bounds[r],
+ * bounds[r + 1]) of every level (bounds: nranks + 1 plane edges, the host's
+ * make_partition parallel.py:87-101) and after each stage the slabs are
+ * exchanged so every rank holds the full level for the next stage:
+ *   ECO_XCHG_P2P   the stage kernel stores its slab into every peer's replica
+ *                  over NVLink (CUDA IPC) + a GPU-side flag barrier;
+ *   ECO_XCHG_NCCL  grouped ncclBroadcast of each slab (the library baseline).
+ * Protocol: create -> info (ECO_SLAB_INFO_BYTES per rank) -> all-gather the
+ * infos on the host (any transport) -> connect(all infos, rank order) ->
+ * solve (collective: every rank calls it with the same problem).  solve
+ * writes the full J stack (H + 1 levels, NULL to skip) and this rank's
+ * policy slab P_slab (H, hi - lo, n_soc, n_t) (NULL to skip). */
+typedef struct EcoSlab EcoSlab;
+#define ECO_XCHG_P2P 0
+#define ECO_XCHG_NCCL 1
+#define ECO_SLAB_INFO_BYTES 256
+int32_t eco_slab_create(int32_t nranks, int32_t rank, int32_t exchange,
+                        const int32_t* bounds, int32_t precision,
+                        int32_t n_v, int32_t n_soc, int32_t n_t,
+                        int32_t max_horizon, EcoSlab** out);
+int32_t eco_slab_info(EcoSlab* slab, uint8_t* info);
+int32_t eco_slab_connect(EcoSlab* slab, const uint8_t* all_info);
+int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant,
+                       const EcoProblem* prob, const EcoStepPlan* plans,
+                       int32_t H, const double* terminal, double* J_stack,
+                       int32_t* P_slab, int32_t count_live, EcoStats* stats);
+int32_t eco_slab_destroy(EcoSlab* slab);
 
 #ifdef __cplusplus
 }

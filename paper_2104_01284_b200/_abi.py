@@ -21,7 +21,9 @@ MAX_GEARS = 16
 MAX_AXIS = 32
 MAX_MAP = MAX_AXIS * MAX_AXIS
 MAX_WINDOWS = 8
-ABI_VERSION = 2
+ABI_VERSION = 3
+XCHG_P2P, XCHG_NCCL = 0, 1
+SLAB_INFO_BYTES = 256
 
 OK, ERR_ARG, ERR_CUDA, ERR_NODEV = 0, 1, 2, 3
 FP32, FP64 = 0, 1
@@ -238,6 +240,12 @@ def _declare(lib):
         "eco_batch_create": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), P(C.c_void_p)]),
         "eco_batch_solve": (_I, [C.c_void_p, _I, C.c_void_p, _PI, _PD, _PD, _PI, _I, P(EcoStats)]),
         "eco_batch_destroy": (_I, [C.c_void_p]),
+        "eco_slab_create": (_I, [_I, _I, _I, _PI, _I, _I, _I, _I, _I, P(C.c_void_p)]),
+        "eco_slab_info": (_I, [C.c_void_p, C.c_void_p]),
+        "eco_slab_connect": (_I, [C.c_void_p, C.c_void_p]),
+        "eco_slab_solve": (_I, [C.c_void_p, P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI, _I,
+                                P(EcoStats)]),
+        "eco_slab_destroy": (_I, [C.c_void_p]),
         "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _I, C.c_void_p, _PI, _PD, _PD, _PI,
                                  P(EcoStats)]),
     }

@@ -12,7 +12,10 @@
 #include <string>
 #include <algorithm>
 #include <memory>
+#include <stdexcept>
 #include <vector>
+
+#include <nccl.h>
 
 #include "eco_kernels.cuh"
 #include "eco_mpc.cuh"
@@ -185,6 +188,7 @@ struct Geometry {
     int h_gmax[4] = {0, 0, 0, 0};     // max feasible actions of a plane
     int64_t rows_total = 0;
     int tj = 0, nchunk = 0, band_cap = 0;   // stage-kernel tile shape the plans were built for
+    int plo = 0, phi = -1;                  // tiles of planes [plo, phi) ordered first (slab solves)
 
     void alloc(int P, int nv, int U) {
         const size_t np = (size_t)P * nv * U;
@@ -237,7 +241,8 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     if (G.tiles.n != ntiles) G.tiles.alloc(ntiles);
     if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
     if (G.order.n != ntiles) { G.order.alloc(ntiles); G.rank_of.alloc(ntiles); }
-    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.tj, g.nx, G.order.p, G.rank_of.p);
+    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, G.phi < 0 ? g.nv : G.phi,
+                                           G.order.p, G.rank_of.p);
     ECO_CUDA(cudaGetLastError());
     dim3 tgrid(g.nv * G.nchunk, g.P);
     geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
@@ -344,8 +349,8 @@ void set_smem_attr(K kernel, size_t smem) {
 }
 
 template <typename Real, int MODE>
-void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st) {
-    const unsigned grid = (unsigned)(a.nv * tc.nchunk);
+void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st, int ntiles = -1) {
+    const unsigned grid = (unsigned)(ntiles >= 0 ? ntiles : a.nv * tc.nchunk);
     const unsigned block = (unsigned)(tc.S * tc.slices);
     if (MODE == 0) {
         auto k = tc.wide ? (count ? bellman_wide_kernel<Real, true> : bellman_wide_kernel<Real, false>)
@@ -468,6 +473,48 @@ struct TablesDev {
 };
 
 // --------------------------------------------------------- horizon solve
+// Per-solve inputs of a horizon solve on the device: plant, the H step
+// plans (DevPlan + source speed axis + ladders) and the axes.
+struct HorizonInputs {
+    DBuf<EcoPlant> plant;
+    DBuf<DevPlan> plans;
+    DBuf<double> v, tdep, wait, te, tb, soc;
+    DBuf<uint8_t> green, dep;
+    void upload(const EcoPlant* p, const EcoProblem* pr, const EcoStepPlan* pl, int H, cudaStream_t st) {
+        const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t;
+        std::vector<DevPlan> hp(H);
+        std::vector<double> hv((size_t)H * nv);
+        std::vector<uint8_t> hgreen((size_t)H * nt), hdep((size_t)H * nt);
+        std::vector<double> htdep((size_t)H * nt), hwait((size_t)H * nt);
+        for (int k = 0; k < H; ++k) {
+            const EcoStepPlan& s = pl[k];
+            if (!s.v_src || !s.arr_green || !s.dep_ok || !s.t_dep || !s.wait) throw ArgError{"null plan array"};
+            hp[k] = dev_plan(s);
+            std::memcpy(&hv[(size_t)k * nv], s.v_src, sizeof(double) * nv);
+            std::memcpy(&hgreen[(size_t)k * nt], s.arr_green, nt);
+            std::memcpy(&hdep[(size_t)k * nt], s.dep_ok, nt);
+            std::memcpy(&htdep[(size_t)k * nt], s.t_dep, sizeof(double) * nt);
+            std::memcpy(&hwait[(size_t)k * nt], s.wait, sizeof(double) * nt);
+        }
+        plant.ensure(1);
+        plant.upload(p, 1, st);
+        plans.ensure(H); v.ensure((size_t)H * nv); tdep.ensure((size_t)H * nt); wait.ensure((size_t)H * nt);
+        green.ensure((size_t)H * nt); dep.ensure((size_t)H * nt);
+        te.ensure(pr->n_te); tb.ensure(pr->n_tb); soc.ensure(nx);
+        plans.upload(hp.data(), H, st);
+        v.upload(hv.data(), hv.size(), st);
+        green.upload(hgreen.data(), hgreen.size(), st);
+        dep.upload(hdep.data(), hdep.size(), st);
+        tdep.upload(htdep.data(), htdep.size(), st);
+        wait.upload(hwait.data(), hwait.size(), st);
+        te.upload(pr->te_axis, pr->n_te, st);
+        tb.upload(pr->tb_axis, pr->n_tb, st);
+        soc.upload(pr->soc_axis, nx, st);
+        // pageable sources: the copies must finish before the vectors go
+        ECO_CUDA(cudaStreamSynchronize(st));
+    }
+};
+
 template <typename Real>
 struct HorizonWorkspace {
     Geometry<Real> G;
@@ -497,35 +544,12 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     const size_t ns = (size_t)nv * nx * nt;
     cudaStream_t st = 0;
     int64_t launches = 0;
-    DBuf<EcoPlant> d_plant(1);
-    d_plant.upload(plant, 1, st);
-    std::vector<DevPlan> hp(H);
-    std::vector<double> hv((size_t)H * nv);
-    std::vector<uint8_t> hgreen((size_t)H * nt), hdep((size_t)H * nt);
-    std::vector<double> htdep((size_t)H * nt), hwait((size_t)H * nt);
-    for (int k = 0; k < H; ++k) {
-        const EcoStepPlan& s = plans[k];
-        if (!s.v_src || !s.arr_green || !s.dep_ok || !s.t_dep || !s.wait) throw ArgError{"null plan array"};
-        hp[k] = dev_plan(s);
-        std::memcpy(&hv[(size_t)k * nv], s.v_src, sizeof(double) * nv);
-        std::memcpy(&hgreen[(size_t)k * nt], s.arr_green, nt);
-        std::memcpy(&hdep[(size_t)k * nt], s.dep_ok, nt);
-        std::memcpy(&htdep[(size_t)k * nt], s.t_dep, sizeof(double) * nt);
-        std::memcpy(&hwait[(size_t)k * nt], s.wait, sizeof(double) * nt);
-    }
-    DBuf<DevPlan> d_plans(H);
-    DBuf<double> d_v((size_t)H * nv), d_tdep((size_t)H * nt), d_wait((size_t)H * nt);
-    DBuf<uint8_t> d_green((size_t)H * nt), d_dep((size_t)H * nt);
-    DBuf<double> d_te(pr->n_te), d_tb(pr->n_tb), d_soc(nx);
-    d_plans.upload(hp.data(), H, st);
-    d_v.upload(hv.data(), hv.size(), st);
-    d_green.upload(hgreen.data(), hgreen.size(), st);
-    d_dep.upload(hdep.data(), hdep.size(), st);
-    d_tdep.upload(htdep.data(), htdep.size(), st);
-    d_wait.upload(hwait.data(), hwait.size(), st);
-    d_te.upload(pr->te_axis, pr->n_te, st);
-    d_tb.upload(pr->tb_axis, pr->n_tb, st);
-    d_soc.upload(pr->soc_axis, nx, st);
+    HorizonInputs in;
+    in.upload(plant, pr, plans, H, st);
+    DBuf<EcoPlant>& d_plant = in.plant;
+    DBuf<DevPlan>& d_plans = in.plans;
+    DBuf<double>&d_v = in.v, &d_tdep = in.tdep, &d_wait = in.wait, &d_te = in.te, &d_tb = in.tb, &d_soc = in.soc;
+    DBuf<uint8_t>&d_green = in.green, &d_dep = in.dep;
     TablesDev tdev;   // plant path: no tables
 
     // device buffers persist across calls (grow-only workspace): repeated
@@ -1321,6 +1345,242 @@ BatchBase* make_batch(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* 
     return b;
 }
 
+// ---------------------------------------------------------------- slabs
+// Slab-partitioned horizon solve (C5): rank g of G computes the
+// speed planes [lo_g, hi_g) of every level (make_partition, parallel.py:87-101)
+// reading the full J_{k+1}; after each stage the slabs are exchanged so every
+// rank again holds the full level.
+//   ECO_XCHG_P2P  the stage kernel's epilogue stores its slab straight into
+//                 every peer's replica over NVLink (CUDA IPC), followed by a
+//                 flag barrier across the GPUs (slab_barrier_kernel);
+//   ECO_XCHG_NCCL one grouped ncclBroadcast per slab after the stage kernel.
+// Policies stay sharded: each rank returns its own planes.
+constexpr int kSlabInfoBytes = 256;     // [J handle 64][flag handle 64][nccl id 128]
+
+struct SlabBase {
+    int precision = 0;
+    virtual ~SlabBase() = default;
+    virtual void info(unsigned char* out) = 0;
+    virtual void connect(const unsigned char* all) = 0;
+    virtual void solve(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H,
+                       const double* terminal, double* J_stack, int32_t* P_slab, int count, EcoStats* stats) = 0;
+};
+
+template <typename Real>
+struct Slab : SlabBase {
+    int nranks, rank, exchange, Hmax;
+    int nv, nx, nt;
+    size_t ns, LV, LC;
+    std::vector<int> lo, hi;
+    DBuf<Real> J;                      // (Hmax + 1) levels, IPC-exported
+    DBuf<unsigned> flag;               // barrier counter, IPC-exported
+    DBuf<int> err;
+    DBuf<int32_t> P;
+    DBuf<double> tmp;
+    DBuf<unsigned long long> live;
+    Geometry<Real> G;
+    std::vector<Real*> peer_J;         // opened replicas (excluding self)
+    std::vector<unsigned*> peer_flag;
+    DBuf<Real*> d_peer_J;
+    DBuf<unsigned*> d_peer_flag;
+    unsigned long long barriers = 0;
+    ncclComm_t comm = nullptr;
+    ncclUniqueId nid{};
+    bool connected = false;
+    cudaStream_t st = 0;
+
+    Slab(int nranks_, int rank_, int exchange_, const int32_t* bounds, int nv_, int nx_, int nt_, int Hmax_)
+        : nranks(nranks_), rank(rank_), exchange(exchange_), Hmax(Hmax_), nv(nv_), nx(nx_), nt(nt_) {
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ArgError{"invalid rank / world size"};
+        if (exchange != ECO_XCHG_P2P && exchange != ECO_XCHG_NCCL) throw ArgError{"unknown exchange mode"};
+        // the host's make_partition (parallel.py:87-101): contiguous,
+        // non-empty, covering [0, n_v)
+        if (bounds[0] != 0 || bounds[nranks] != nv) throw ArgError{"partition does not cover the speed planes"};
+        lo.resize(nranks); hi.resize(nranks);
+        for (int g = 0; g < nranks; ++g) {
+            lo[g] = bounds[g];
+            hi[g] = bounds[g + 1];
+            if (hi[g] <= lo[g]) throw ArgError{"partition ranges must be non-empty and ordered"};
+        }
+        ns = (size_t)nv * nx * nt;
+        LV = level_stride(ns);
+        LC = level_copy(ns);
+        J.alloc((size_t)(Hmax + 1) * LV);
+        flag.alloc(1);
+        ECO_CUDA(cudaMemset(flag.p, 0, sizeof(unsigned)));
+        err.alloc(1);
+        ECO_CUDA(cudaMemset(err.p, 0, sizeof(int)));
+        live.alloc(1);
+        if (exchange == ECO_XCHG_NCCL && rank == 0) {
+            if (ncclGetUniqueId(&nid) != ncclSuccess) throw std::runtime_error("ncclGetUniqueId failed");
+        }
+        ECO_CUDA(cudaStreamCreate(&st));
+    }
+    ~Slab() override {
+        if (comm) ncclCommDestroy(comm);
+        for (Real* p : peer_J) cudaIpcCloseMemHandle(p);
+        for (unsigned* p : peer_flag) cudaIpcCloseMemHandle(p);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    void info(unsigned char* out) override {
+        std::memset(out, 0, kSlabInfoBytes);
+        cudaIpcMemHandle_t hj{}, hf{};
+        if (exchange == ECO_XCHG_P2P && nranks > 1) {
+            ECO_CUDA(cudaIpcGetMemHandle(&hj, J.p));
+            ECO_CUDA(cudaIpcGetMemHandle(&hf, flag.p));
+        }
+        std::memcpy(out, &hj, sizeof hj);
+        std::memcpy(out + 64, &hf, sizeof hf);
+        std::memcpy(out + 128, &nid, sizeof nid);
+    }
+
+    void connect(const unsigned char* all) override {
+        if (connected) throw ArgError{"slab session already connected"};
+        if (exchange == ECO_XCHG_P2P) {
+            for (int g = 0; g < nranks; ++g) {
+                if (g == rank) continue;
+                cudaIpcMemHandle_t hj, hf;
+                std::memcpy(&hj, all + (size_t)g * kSlabInfoBytes, sizeof hj);
+                std::memcpy(&hf, all + (size_t)g * kSlabInfoBytes + 64, sizeof hf);
+                void* pj = nullptr;
+                void* pf = nullptr;
+                ECO_CUDA(cudaIpcOpenMemHandle(&pj, hj, cudaIpcMemLazyEnablePeerAccess));
+                ECO_CUDA(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
+                peer_J.push_back(static_cast<Real*>(pj));
+                peer_flag.push_back(static_cast<unsigned*>(pf));
+            }
+            if (!peer_J.empty()) {
+                d_peer_J.alloc(peer_J.size());
+                d_peer_J.upload(peer_J.data(), peer_J.size(), st);
+                d_peer_flag.alloc(peer_flag.size());
+                d_peer_flag.upload(peer_flag.data(), peer_flag.size(), st);
+            }
+        } else {
+            std::memcpy(&nid, all + 128, sizeof nid);      // rank 0's id
+            if (ncclCommInitRank(&comm, nranks, nid, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
+        }
+        ECO_CUDA(cudaStreamSynchronize(st));
+        connected = true;
+    }
+
+    void exchange_level(int k) {
+        Real* Lk = J.p + (size_t)k * LV;
+        const size_t plane = (size_t)nx * nt;
+        if (exchange == ECO_XCHG_P2P) {
+            ++barriers;
+            slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
+                                                  (unsigned)(barriers * nranks), err.p);
+            ECO_CUDA(cudaGetLastError());
+            return;
+        }
+        const ncclDataType_t ty = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
+        if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+        for (int g = 0; g < nranks; ++g) {
+            const size_t o0 = (size_t)lo[g] * plane, n0 = (size_t)(hi[g] - lo[g]) * plane;
+            if (!n0) continue;
+            // copy 0 and its shifted twin (copy 1 holds J[i + 1] at i)
+            const size_t a1 = o0 ? o0 - 1 : 0, b1 = o0 + n0 - 1;
+            if (ncclBroadcast(Lk + o0, Lk + o0, n0, ty, g, comm, st) != ncclSuccess ||
+                ncclBroadcast(Lk + LC + a1, Lk + LC + a1, b1 - a1, ty, g, comm, st) != ncclSuccess)
+                throw std::runtime_error("ncclBroadcast failed");
+        }
+        if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
+    }
+
+    void solve(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H, const double* terminal,
+               double* J_stack, int32_t* P_slab, int count, EcoStats* stats) override {
+        if (!connected) throw ArgError{"slab session not connected"};
+        if (pr->n_v != nv || pr->n_soc != nx || pr->n_t != nt) throw ArgError{"grid differs from the slab session"};
+        if (H < 1 || H > Hmax) throw ArgError{"horizon exceeds the slab session's capacity"};
+        const int U = pr->n_te * pr->n_tb;
+        const int plo = lo[rank], phi = hi[rank];
+        const size_t plane = (size_t)nx * nt, slab_ns = (size_t)(phi - plo) * plane;
+        int64_t launches = 0;
+        HorizonInputs in;
+        in.upload(plant, pr, plans, H, st);
+        P.ensure((size_t)H * slab_ns);
+        tmp.ensure(ns * (size_t)(J_stack ? H + 1 : 1));
+        tmp.upload(terminal, ns, st);
+        ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
+        EventTimer all, sweep;
+        all.start(st);
+        G.dims = GeomDims{H, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
+        G.plo = plo;
+        G.phi = phi;
+        TablesDev tdev;
+        build_geometry(G, in.plant.p, in.plans.p, in.v.p, in.te.p, in.tb.p, in.soc.p, tdev.view, st, &launches);
+        to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(tmp.p, J.p + (size_t)H * LV, ns, pr->j_inf);
+        ECO_CUDA(cudaGetLastError());
+        ++launches;
+        const TileCfg tc = tile_cfg(G, nt, 0);
+        sweep.start(st);
+        for (int k = H - 1; k >= 0; --k) {
+            StageArgs<Real> a = stage_args(G, k, in.v.p + (size_t)k * nv, nt, tc);
+            a.green = in.green.p + (size_t)k * nt;
+            a.dep_ok = in.dep.p + (size_t)k * nt;
+            a.t_dep = in.tdep.p + (size_t)k * nt;
+            a.wait = in.wait.p + (size_t)k * nt;
+            a.J_next = J.p + (size_t)(k + 1) * LV;
+            a.J_next1 = a.J_next + LC;
+            a.J_out = J.p + (size_t)k * LV;
+            a.J_out1 = a.J_out + LC;
+            // the kernel indexes P by the global state: shift the slab buffer
+            a.P_out = P.p + (size_t)k * slab_ns - (ptrdiff_t)((size_t)plo * plane);
+            a.live = count ? live.p : nullptr;
+            a.src_kind = plans[k].src_kind;
+            a.t0 = pr->t0;
+            a.dtg = pr->dtg;
+            a.j_inf = (Real)pr->j_inf;
+            if (exchange == ECO_XCHG_P2P && !peer_J.empty()) {
+                a.peer_base = d_peer_J.p;
+                a.npeer = (int)peer_J.size();
+                a.peer_off = (size_t)k * LV;
+                a.lc = LC;
+            }
+            launch_stage<Real, 0>(a, tc, count, st, (phi - plo) * tc.nchunk);
+            ++launches;
+            if (nranks > 1) {
+                exchange_level(k);
+                ++launches;
+            }
+        }
+        sweep.stop(st);
+        if (J_stack) {
+            to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(J.p, tmp.p, ns, H + 1,
+                                                                                   pr->j_inf);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
+        }
+        all.stop(st);
+        if (J_stack) tmp.download(J_stack, ns * (H + 1), st);
+        if (P_slab) P.download(P_slab, (size_t)H * slab_ns, st);
+        int herr = 0;
+        unsigned long long nlive = 0;
+        ECO_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaMemcpyAsync(&nlive, live.p, sizeof nlive, cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaStreamSynchronize(st));
+        if (herr) throw std::runtime_error("slab barrier timed out (a peer rank stopped)");
+        if (stats) {
+            stats->device_ms = all.ms();
+            stats->dominant_ms = sweep.ms();
+            stats->dense_updates = (int64_t)slab_ns * U * H;
+            stats->live_updates = count ? (int64_t)nlive : -1;
+            stats->stages = H;
+            stats->kernel_launches = launches;
+        }
+    }
+};
+
+SlabBase* make_slab(int nranks, int rank, int exchange, const int32_t* bounds, int precision, int nv, int nx, int nt,
+                    int Hmax) {
+    SlabBase* s;
+    if (precision == ECO_FP64) s = new Slab<double>(nranks, rank, exchange, bounds, nv, nx, nt, Hmax);
+    else s = new Slab<float>(nranks, rank, exchange, bounds, nv, nx, nt, Hmax);
+    s->precision = precision;
+    return s;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -1487,6 +1747,48 @@ int32_t eco_solve_batch(const EcoPlant* plant, const EcoRoute* route, const EcoM
         std::unique_ptr<BatchBase> b(make_batch(plant, route, cfg));
         b->solve(n_scen, timings, s, t_start, J0, P0, 0, stats);
     });
+}
+
+int32_t eco_slab_create(int32_t nranks, int32_t rank, int32_t exchange, const int32_t* bounds, int32_t precision,
+                        int32_t n_v, int32_t n_soc, int32_t n_t, int32_t max_horizon, EcoSlab** out) {
+    return run_guarded([&] {
+        if (!out || !bounds) throw ArgError{"null pointer argument"};
+        if (n_v < 2 || n_soc < 2 || n_t < 2 || max_horizon < 1) throw ArgError{"invalid grid / horizon"};
+        if (nranks < 1) throw ArgError{"invalid rank / world size"};
+        *out = reinterpret_cast<EcoSlab*>(make_slab(nranks, rank, exchange, bounds, precision, n_v, n_soc, n_t,
+                                                    max_horizon));
+    });
+}
+
+int32_t eco_slab_info(EcoSlab* slab, uint8_t* info) {
+    return run_guarded([&] {
+        if (!slab || !info) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SlabBase*>(slab)->info(info);
+    });
+}
+
+int32_t eco_slab_connect(EcoSlab* slab, const uint8_t* all_info) {
+    return run_guarded([&] {
+        if (!slab || !all_info) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SlabBase*>(slab)->connect(all_info);
+    });
+}
+
+int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant, const EcoProblem* prob, const EcoStepPlan* plans,
+                       int32_t H, const double* terminal, double* J_stack, int32_t* P_slab, int32_t count_live,
+                       EcoStats* stats) {
+    return run_guarded([&] {
+        check_plant(plant);
+        check_problem(prob);
+        if (!slab || !plans || !terminal) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SlabBase*>(slab)->solve(plant, prob, plans, H, terminal, J_stack, P_slab, count_live,
+                                                 stats);
+    });
+}
+
+int32_t eco_slab_destroy(EcoSlab* slab) {
+    delete reinterpret_cast<SlabBase*>(slab);
+    return ECO_OK;
 }
 
 }  // extern "C"

@@ -350,17 +350,22 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
 // per plan: tiles heaviest first -- planes by descending feasible-action
 // count (ties by plane index), the SoC chunks of a plane consecutively.  The
 // order only balances the load; results do not depend on it.
-__global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int tj, int nx,
+// A slab-partitioned solve (C5) orders the tiles of its own planes
+// [plo, phi) first, so a launch of (phi - plo) * nchunk CTAs covers exactly
+// the slab.
+__global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int plo, int phi,
                                   int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
     const int p = blockIdx.x;
     const int32_t* c = count + (size_t)p * nv;
     const size_t base = (size_t)p * nv * nchunk;
     for (int iv = threadIdx.x; iv < nv; iv += blockDim.x) {
         const int w = c[iv];
+        const bool in = iv >= plo && iv < phi;
         int r = 0;
         for (int j = 0; j < nv; ++j) {
             const int wj = c[j];
-            r += (wj > w) || (wj == w && j < iv);
+            const bool jin = j >= plo && j < phi;
+            r += (jin && !in) || (jin == in && ((wj > w) || (wj == w && j < iv)));
         }
         for (int ch = 0; ch < nchunk; ++ch) {
             const int rank = r * nchunk + ch;
@@ -368,7 +373,29 @@ __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int
             rank_of[base + iv * nchunk + ch] = rank;
         }
     }
-    (void)tj; (void)nx;
+}
+
+// Cross-GPU stage barrier of the P2P slab exchange: every rank's stage
+// kernel has stored its slab into all replicas (kernel boundary + system
+// fence), then bumps every rank's counter and waits for its own to reach
+// `target`.  Bounded: after 20 s it records a timeout instead of hanging.
+__global__ void slab_barrier_kernel(unsigned* const* __restrict__ peer_flags, int npeer, unsigned* flag,
+                                    unsigned target, int* error) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    for (int g = 0; g < npeer; ++g) atomicAdd_system(peer_flags[g], 1u);
+    atomicAdd_system(flag, 1u);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        const unsigned v = atomicAdd_system(flag, 0u);
+        if (v >= target) break;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) { *error = 1; break; }
+        __nanosleep(200);
+    }
+    __threadfence_system();
 }
 
 // ---------------------------------------------------------- stage sweep
@@ -407,6 +434,10 @@ struct StageArgs {
     int tj, nchunk, S, slices;    // tile: tj SoC rows; S threads per action slice
     int count_max, band_cap;      // staging capacity: actions per plane, band elements
     int wide;                     // > 0: wide-row path, warps per row (n_t >= 128)
+    Real* const* peer_base;       // C5 P2P exchange: level-0 base of each peer replica (device array)
+    int npeer;
+    size_t peer_off;              // this stage's level offset in a replica
+    size_t lc;                    // copy-1 offset within a level
     int src_kind;
     double t0, dtg, gamma, dwell;
     Real j_inf;
@@ -511,6 +542,17 @@ struct TileSmem {
 // copies of J_next (as-is / shifted by one) make every corner pair one aligned
 // 64-bit load.  Standstill planes (v == 0: red-wait / dwell relocation,
 // K:519-535) run a per-state loop.
+// C5 P2P exchange: the slab's outputs go straight into every peer's replica
+// of the level (NVLink stores), both copies.
+template <typename Real>
+__device__ __forceinline__ void store_peers(const StageArgs<Real>& a, size_t i, Real val) {
+    for (int g = 0; g < a.npeer; ++g) {
+        Real* pb = a.peer_base[g] + a.peer_off;
+        pb[i] = val;
+        if (i > 0) pb[a.lc + i - 1] = val;
+    }
+}
+
 template <typename Real, bool COUNT, bool WIDE = false>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
@@ -533,6 +575,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
             a.J_out[obase + f] = (Real)INFINITY;
             if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
             if (a.P_out) a.P_out[obase + f] = -1;
+            store_peers(a, obase + f, (Real)INFINITY);
         }
         return;
     }
@@ -966,6 +1009,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
+        store_peers(a, obase + f, val);
         if (a.P_out) a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
     }
     if (dbg) {

@@ -407,3 +407,25 @@ def test_c4_batch_terminal_field_and_no_teleport(vehicle):
                             teleport=False, terminal_field=field.values[s + min(20, route.node_count - 1 - s)])
         J, P = O.solve_context(ctx, parallel=True)
         assert np.array_equal(res.J0[i], J[0]) and np.array_equal(res.P0[i], P[0]), i
+
+
+# ------------------------------------------------------- C5 slab (1 rank)
+
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+@pytest.mark.parametrize("backend", ["b200-fp64", "b200"])
+def test_slab_solver_single_rank_equals_solve_horizon(vehicle, urban_route, exchange, backend):
+    """The slab path on one GPU (world 1) runs the same kernels with the
+    plane-range tile order and the exchange plumbing; results must equal the
+    unpartitioned solve bitwise.  (Multi-rank exchange: tests/test_slab_host.py.)"""
+    from paper_2104_01284_b200.slab import SlabSolver
+    route, spat = urban_route
+    ctx = build_context(vehicle, route, spat, 60, 30.0, grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20)
+    ref = solve_horizon(ctx, backend=backend)
+    with SlabSolver(35, 26, 40, 20, backend=backend, exchange=exchange, rank=0, world=1) as ss:
+        for _ in range(2):
+            res = ss.solve(ctx, return_J=True)
+            assert res.planes == (0, 35)
+            for k in range(21):
+                assert np.array_equal(res.J[k], ref.tables[k].values), k
+            for k in range(20):
+                assert np.array_equal(res.P[k], ref.policies[k].values), k
