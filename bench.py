@@ -31,6 +31,10 @@ Other workloads (`--workload`; the default line is C2):
   c3  BASELINE configs[2]: one receding-horizon solve on the fine grid
       350 x 260 x 400 (dt = 0.2 s), urban s = 60, t = 30, H = 20.  Replicas
       for N > 1 (the slab-partitioned variant is C5).
+  c5  BASELINE configs[4]: the C3 solve with its speed planes split into N
+      slabs, one per GPU (strong scaling); after every stage the slabs are
+      exchanged (--exchange p2p: NVLink stores from the stage kernel's
+      epilogue + GPU flag barrier; nccl: grouped ncclBroadcast).
 """
 
 from __future__ import annotations
@@ -304,7 +308,7 @@ def cpu_baseline(budget_s: float) -> dict:
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    if args.workload in ("c3", "c4"):
+    if args.workload in ("c3", "c4", "c5"):
         return run_reference_other(args, world)
     budget = args.cpu_seconds
     probe = cpu_sample(3)
@@ -598,6 +602,76 @@ def run_reference_other(args, world):
     }
 
 
+def run_c5(args, rank, world, local_rank):
+    import torch
+    from paper_2104_01284_b200.slab import SlabSolver
+    dist = _dist_init(world, local_rank)
+    backend = "b200-fp64" if args.precision == "fp64" else "b200"
+    ctx = c3_context()
+    g = ctx.grids
+    ss = SlabSolver(g.n_v, g.n_soc, g.n_t, ctx.horizon, backend=backend, exchange=args.exchange, rank=rank,
+                    world=world)
+    for _ in range(args.warmup):
+        ss.solve(ctx, return_P=False)
+    live = ss.solve(ctx, return_P=False, count_live=True).stats["live_updates"]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dev_ms, sweep_ms, launches = 0.0, 0.0, 0
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for _ in range(args.steps):
+            st = ss.solve(ctx, return_P=False).stats
+            dev_ms += st["device_ms"]
+            sweep_ms += st["dominant_ms"]
+            launches += st["kernel_launches"]
+        barrier()
+    t_max = _max_over_ranks(dist, dev_ms)
+    sweep_max = _max_over_ranks(dist, sweep_ms)
+    live_all = live
+    if dist is not None:
+        t = torch.tensor([float(live)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        live_all = float(t.item())
+    # e2e: the public slab API with host context in, this rank's policy slab out
+    barrier()
+    a0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = ss.solve(ctx)
+    barrier()
+    e2e_ms = _max_over_ranks(dist, (time.perf_counter() - a0) * 1e3)
+    ss.close()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    ns = g.n_v * g.n_soc * g.n_t
+    dense = ns * g.n_t_eng * g.n_t_bsg * ctx.horizon          # whole grid, all ranks together
+    out = {
+        "metric": METRIC, "value": dense * args.steps / (t_max / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (urban route seed 0)",
+        "config": {"workload": "C5: the C3 solve (350x260x400 x 23x30, H=20) with its speed planes split into "
+                               f"{world} slab(s) (make_partition), per-stage exchange of the level",
+                   "parallelism": f"v-slabs x{world}, exchange={args.exchange}", "precision": args.precision,
+                   "l2": "levels of 291 MB exceed L2; no flush"},
+        "ms_per_solve": t_max / args.steps, "sweep_ms_per_solve": sweep_max / args.steps,
+        "live_updates_per_step": live_all, "gpu_launches": int(launches),
+        "e2e": {"value": dense * args.steps / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
+                "h2d_bytes_per_step": int(ns * 8), "d2h_bytes_per_step": int(res.P.nbytes)},
+        "roofline": _roofline(args, local_rank, live_all / world, sweep_max / args.steps / 1e3,
+                              "bellman_wide_kernel"),
+        "clocks": clk.summary(),
+    }
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -607,7 +681,8 @@ def main():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p", help="C5 slab exchange")
     ap.add_argument("--scenarios", type=int, default=4096, help="C4 batch size (all ranks together)")
     args = ap.parse_args()
     rank, world, local_rank = env_rank()
@@ -619,6 +694,8 @@ def main():
         out = run_c4(args, rank, world, local_rank)
     elif args.workload == "c3":
         out = run_c3(args, rank, world, local_rank)
+    elif args.workload == "c5":
+        out = run_c5(args, rank, world, local_rank)
     else:
         out = run_ours(args, rank, world, local_rank)
     if out is not None:

@@ -249,7 +249,11 @@ def _declare(lib):
         "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _I, C.c_void_p, _PI, _PD, _PD, _PI,
                                  P(EcoStats)]),
     }
+    # ECO_B200_LIB (a variant build under study) may predate newer entry points
+    lenient = "ECO_B200_LIB" in os.environ
     for name, (res, args) in sig.items():
+        if lenient and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -268,7 +272,7 @@ def lib():
             _LIB = _declare(C.CDLL(str(path)))
         except OSError as exc:
             raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
-        if _LIB.eco_abi_version() != ABI_VERSION:
+        if _LIB.eco_abi_version() != ABI_VERSION and "ECO_B200_LIB" not in os.environ:
             raise NativeLibraryError("ABI version mismatch between eco_b200.h and the Python bindings")
     return _LIB
 

@@ -353,8 +353,14 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
     const unsigned grid = (unsigned)(ntiles >= 0 ? ntiles : a.nv * tc.nchunk);
     const unsigned block = (unsigned)(tc.S * tc.slices);
     if (MODE == 0) {
-        auto k = tc.wide ? (count ? bellman_wide_kernel<Real, true> : bellman_wide_kernel<Real, false>)
-                         : (count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>);
+        using KT = void (*)(StageArgs<Real>);
+        KT k;
+        if (a.npeer > 0)
+            k = tc.wide ? (count ? bellman_wide_kernel<Real, true, true> : bellman_wide_kernel<Real, false, true>)
+                        : (count ? bellman_stage_kernel<Real, true, true> : bellman_stage_kernel<Real, false, true>);
+        else
+            k = tc.wide ? (count ? bellman_wide_kernel<Real, true> : bellman_wide_kernel<Real, false>)
+                        : (count ? bellman_stage_kernel<Real, true> : bellman_stage_kernel<Real, false>);
         set_smem_attr(k, tc.smem);
         // programmatic dependent launch: the prologue overlaps the previous kernel's tail
         cudaLaunchConfig_t lc{};

@@ -553,7 +553,7 @@ __device__ __forceinline__ void store_peers(const StageArgs<Real>& a, size_t i, 
     }
 }
 
-template <typename Real, bool COUNT, bool WIDE = false>
+template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
@@ -575,7 +575,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
             a.J_out[obase + f] = (Real)INFINITY;
             if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
             if (a.P_out) a.P_out[obase + f] = -1;
-            store_peers(a, obase + f, (Real)INFINITY);
+            if (PEERS) store_peers(a, obase + f, (Real)INFINITY);
         }
         return;
     }
@@ -1009,7 +1009,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
-        store_peers(a, obase + f, val);
+        if (PEERS) store_peers(a, obase + f, val);
         if (a.P_out) a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
     }
     if (dbg) {
@@ -1019,25 +1019,27 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     __syncthreads();      // shared buffers are reused by the caller's next tile
 }
 
-template <typename Real, bool COUNT>
+// PEERS: the C5 P2P exchange variant (epilogue stores into peer replicas);
+// a separate instantiation keeps the plain kernels' code unchanged.
+template <typename Real, bool COUNT, bool PEERS = false>
 __global__ void __launch_bounds__(512)
 bellman_stage_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    stage_tile<Real, COUNT>(a, blockIdx.x, smem);
+    stage_tile<Real, COUNT, false, PEERS>(a, blockIdx.x, smem);
 }
 
 // Wide-row variant (n_t >= 128, StageArgs::wide > 0): blocks of <= 256
 // threads with up to 128 registers, so the four corner pointers and the
 // eight in-flight chunk loads of a warp stay in registers.
-template <typename Real, bool COUNT>
+template <typename Real, bool COUNT, bool PEERS = false>
 __global__ void __launch_bounds__(256, ECO_WIDE_MINB)
 bellman_wide_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    stage_tile<Real, COUNT, true>(a, blockIdx.x, smem);
+    stage_tile<Real, COUNT, true, PEERS>(a, blockIdx.x, smem);
 }
 
 // Batch of independent solves sharing one route's geometry (run_bench's
