@@ -182,7 +182,19 @@ __global__ void __launch_bounds__(kDecideThreads)
 mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
                   Ladders lad, const Real* J1, EcoTrajRow* rows) {
     if (st->status != 0) return;
-    const EcoPlant& P = *plant;
+    // the plant (20 KB of maps and axes) is read by every candidate's step
+    // evaluation: one cooperative copy into shared memory
+    __shared__ __align__(16) EcoPlant s_plant;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(plant);
+        uint4* dst = reinterpret_cast<uint4*>(&s_plant);
+        for (int i = threadIdx.x; i < (int)(sizeof(EcoPlant) / 16); i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x == 0)
+            for (int i = (int)(sizeof(EcoPlant) / 16) * 16; i < (int)sizeof(EcoPlant); ++i)
+                reinterpret_cast<char*>(&s_plant)[i] = reinterpret_cast<const char*>(plant)[i];
+    }
+    __syncthreads();
+    const EcoPlant& P = s_plant;
     __shared__ double s_f[kDecideThreads / 32];
     __shared__ int s_u[kDecideThreads / 32];
     __shared__ double s_wait, s_tbase;
