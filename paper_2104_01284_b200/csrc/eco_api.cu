@@ -200,6 +200,9 @@ struct Geometry {
     }
 };
 
+template <typename Real>
+int light_first(const Geometry<Real>& G, int nt, int nlaunch);
+
 // Compacted pair records + SoC row records for P plans (dims filled by the
 // caller).  The row buffer is sized from the feasible-pair count (kept across
 // rebuilds of the same route, so refits allocate nothing).
@@ -241,8 +244,9 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     if (G.tiles.n != ntiles) G.tiles.alloc(ntiles);
     if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
     if (G.order.n != ntiles) { G.order.alloc(ntiles); G.rank_of.alloc(ntiles); }
-    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, G.phi < 0 ? g.nv : G.phi,
-                                           G.order.p, G.rank_of.p);
+    const int phi = G.phi < 0 ? g.nv : G.phi;
+    const int light = light_first<Real>(G, g.nt, (phi - G.plo) * G.nchunk);
+    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, phi, light, G.order.p, G.rank_of.p);
     ECO_CUDA(cudaGetLastError());
     dim3 tgrid(g.nv * G.nchunk, g.P);
     geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
@@ -348,6 +352,22 @@ void set_smem_attr(K kernel, size_t smem) {
     done.emplace_back((const void*)kernel, smem);
 }
 
+inline int sm_count_cached();
+
+// Tiles a stage launch puts in front (geom_order_kernel): when the launch is
+// between one and two waves of resident CTAs, the overflow count.
+template <typename Real>
+int light_first(const Geometry<Real>& G, int nt, int nlaunch) {
+    if (env_int("ECO_LIGHT_FIRST", 1) == 0) return 0;
+    const TileCfg tc = tile_cfg(G, nt, 0);
+    auto k = tc.wide ? bellman_wide_kernel<Real, false> : bellman_stage_kernel<Real, false>;
+    set_smem_attr(k, tc.smem);
+    int per_sm = 0;
+    ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, tc.S * tc.slices, tc.smem));
+    const int slots = per_sm * sm_count_cached();
+    return (slots > 0 && nlaunch > slots && nlaunch < 2 * slots) ? nlaunch - slots : 0;
+}
+
 template <typename Real, int MODE>
 void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st, int ntiles = -1) {
     const unsigned grid = (unsigned)(ntiles >= 0 ? ntiles : a.nv * tc.nchunk);
@@ -393,6 +413,16 @@ struct SolveSync {
         if (tile_ctr.n < (size_t)H) tile_ctr.alloc(H);
     }
 };
+
+inline int sm_count_cached() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        ECO_CUDA(cudaGetDevice(&dev));
+        ECO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
 
 inline int sm_count() {
     static int n = 0;

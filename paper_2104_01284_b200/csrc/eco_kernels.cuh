@@ -352,12 +352,16 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
 // order only balances the load; results do not depend on it.
 // A slab-partitioned solve (C5) orders the tiles of its own planes
 // [plo, phi) first, so a launch of (phi - plo) * nchunk CTAs covers exactly
-// the slab.
+// the slab.  light > 0 (a launch slightly larger than one wave of resident
+// CTAs): the `light` lightest launched tiles go first -- they finish early and
+// free their slots for the tail of the heavy ones, instead of forming a
+// second wave behind the heaviest tiles.
 __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int plo, int phi,
-                                  int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
+                                  int light, int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
     const int p = blockIdx.x;
     const int32_t* c = count + (size_t)p * nv;
     const size_t base = (size_t)p * nv * nchunk;
+    const int nlaunch = (phi - plo) * nchunk;
     for (int iv = threadIdx.x; iv < nv; iv += blockDim.x) {
         const int w = c[iv];
         const bool in = iv >= plo && iv < phi;
@@ -368,7 +372,9 @@ __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int
             r += (jin && !in) || (jin == in && ((wj > w) || (wj == w && j < iv)));
         }
         for (int ch = 0; ch < nchunk; ++ch) {
-            const int rank = r * nchunk + ch;
+            int rank = r * nchunk + ch;
+            if (light > 0 && rank < nlaunch)
+                rank = rank >= nlaunch - light ? rank - (nlaunch - light) : rank + light;
             order[base + rank] = iv * nchunk + ch;
             rank_of[base + iv * nchunk + ch] = rank;
         }
