@@ -124,6 +124,10 @@ def loop_short():
     traj = simulate_closed_loop(route, spat, mpc)
     np.savez_compressed(HERE / "loop_short_small.npz", rows=traj_array(traj),
                         final=np.array([traj.final_state.v, traj.final_state.soc, traj.final_state.t]))
+    # the reference's own byte-deterministic writers (io.py) on this run
+    from ecodrive import io as rio
+    rio.write_trajectory_csv(HERE / "loop_short_small_traj.csv", traj)
+    rio.write_summary_json(HERE / "loop_short_small_summary.json", rio.summarize(traj))
 
 
 def loop_urban():

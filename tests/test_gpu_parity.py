@@ -429,3 +429,22 @@ def test_slab_solver_single_rank_equals_solve_horizon(vehicle, urban_route, exch
                 assert np.array_equal(res.J[k], ref.tables[k].values), k
             for k in range(20):
                 assert np.array_equal(res.P[k], ref.policies[k].values), k
+
+
+def test_closed_loop_files_byte_identical_to_reference(vehicle, short_route, tmp_path):
+    """The fp64 device loop written with io.py's format: the trajectory CSV is
+    byte-identical to the reference's file; the summary differs only in the
+    backend name."""
+    import json
+    from conftest import GOLDEN
+    from paper_2104_01284_b200.io import summarize, write_summary_json, write_trajectory_csv
+    route, spat = short_route
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=SMALL, penalty=PEN, horizon=8, backend="b200-fp64").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    write_trajectory_csv(tmp_path / "t.csv", traj)
+    assert (tmp_path / "t.csv").read_bytes() == (GOLDEN / "loop_short_small_traj.csv").read_bytes()
+    write_summary_json(tmp_path / "s.json", summarize(traj))
+    ours = json.loads((tmp_path / "s.json").read_text())
+    ref = json.loads((GOLDEN / "loop_short_small_summary.json").read_text())
+    assert ours.pop("backend") == "b200-fp64" and ref.pop("backend") == "parallel"
+    assert ours == ref
