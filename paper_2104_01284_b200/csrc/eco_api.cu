@@ -261,12 +261,13 @@ struct TileCfg {
     int tj, nchunk, S, slices;
     int count_max = 0, band_cap = 0;
     int wide = 0;
+    int alias = 0;
     size_t smem;
 };
 
 
 template <typename Real>
-TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode) {
+TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode, bool alias = false) {
     const int nx = G.dims.nx;
     TileCfg t{};
     if (mode == 1) {
@@ -299,7 +300,8 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode) {
         t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", std::max(1, 256 / t.S)), 512 / t.S));
         t.count_max = std::max(1, G.h_gmax[0]);
         t.band_cap = G.band_cap;
-        t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, t.band_cap).total;
+        t.alias = alias ? 1 : 0;
+        t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, t.band_cap, alias).total;
     }
     if (t.smem > 227 * 1024) throw ArgError{"tile reduction buffers exceed shared memory"};
     return t;
@@ -332,6 +334,7 @@ StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int n
     a.count_max = tc.count_max;
     a.band_cap = tc.band_cap;
     a.wide = tc.wide;
+    a.alias = tc.alias;
     a.gamma = g.gamma;
     return a;
 }
@@ -1281,7 +1284,7 @@ struct Batch : BatchBase {
             fitted = true;
         }
         const int chunk = std::max(1, std::min(env_int("ECO_BATCH_CHUNK", 4096), 65535));
-        const TileCfg tc = tile_cfg(ctx.G, nt, 0);
+        const TileCfg tc = tile_cfg(ctx.G, nt, 0, env_int("ECO_BATCH_ALIAS", 1) != 0);
         const size_t LV = level_stride(ns), LC = level_copy(ns);
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};

@@ -440,6 +440,7 @@ struct StageArgs {
     int tj, nchunk, S, slices;    // tile: tj SoC rows; S threads per action slice
     int count_max, band_cap;      // staging capacity: actions per plane, band elements
     int wide;                     // > 0: wide-row path, warps per row (n_t >= 128)
+    int alias;                    // reduction buffers alias the staging region (TileSmem)
     Real* const* peer_base;       // C5 P2P exchange: level-0 base of each peer replica (device array)
     int npeer;
     size_t peer_off;              // this stage's level offset in a replica
@@ -531,17 +532,25 @@ constexpr int kMW = ECO_WIDE_CHUNKS;   // wide path: 64-state chunks per warp
 template <typename Real>
 struct TileSmem {
     size_t green, red_best, red_arg, rr, act, band, total;
-    __host__ __device__ TileSmem(int nt, int tj, int slices, int count_max, int band_cap) {
+    // alias: the slice-reduction buffers reuse the staging region (row
+    // records + J band), dead once the action loop is over (the staged path
+    // writes them after a barrier); the action records stay live for the
+    // merge.  Smaller CTAs -> 4 per SM: used by the (throughput-bound) batch
+    // kernel; the single-solve kernels keep one wave of 3 per SM.
+    __host__ __device__ TileSmem(int nt, int tj, int slices, int count_max, int band_cap, bool alias = false) {
         size_t o = 0;
         green = o;    o = align16(o + (size_t)nt);
+        act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
+        const size_t red0 = o;
         red_best = o; o = align16(o + (size_t)slices * tj * nt * sizeof(Real));
         red_arg = o;  o = align16(o + (size_t)slices * tj * nt * sizeof(int32_t));
+        const size_t red_end = o;
+        if (alias) o = red0;
         rr = o;       o = align16(o + (size_t)count_max * tj *
                                   (sizeof(RowRec2<Real>) > sizeof(RowRec<Real>) ? sizeof(RowRec2<Real>)
                                                                                  : sizeof(RowRec<Real>)));
-        act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
         band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
-        total = o;
+        total = o > red_end ? o : red_end;
     }
 };
 
@@ -594,7 +603,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         return;
     }
     const double v = tp->moving ? 1.0 : 0.0;       // only its sign is used below
-    const TileSmem<Real> L(nt, a.tj, a.slices, a.count_max, a.band_cap);
+    const TileSmem<Real> L(nt, a.tj, a.slices, a.count_max, a.band_cap, a.alias != 0);
     uint8_t* s_green = smem + L.green;
     Real* s_best = (Real*)(smem + L.red_best);
     int32_t* s_arg = (int32_t*)(smem + L.red_arg);
@@ -737,6 +746,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 }
             }
         }
+        if (a.alias) __syncthreads();      // the reduction buffers alias the staging region
 #pragma unroll
         for (int i = 0; i < kZP; ++i) {
             const int z = z0 + i;
