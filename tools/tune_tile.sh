@@ -1,6 +1,6 @@
 #!/bin/bash
 # Per-stage sweep time of the C2 workload for several tile shapes / band caps.
-CFGS=("2 16 40" "2 16 36")
+CFGS=("2 16 40" "4 8 40" "3 8 40" "2 12 40")
 for cfg in "${CFGS[@]}"; do
   set -- $cfg
   ECO_TILE_TJ=$1 ECO_TILE_SLICES=$2 ECO_BAND_KB=$3 python tools/profile_c2.py --steps 20 > /tmp/t.log 2>&1
