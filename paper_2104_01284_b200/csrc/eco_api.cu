@@ -841,10 +841,19 @@ __global__ void field_init_kernel(const double* soc, const double* v_end, int nv
 }
 
 // build_terminal_cost mpc.py:96-158 on the device: N-1 (v, soc) sweeps.
+// Replayable capture of the N-1 field launches (per session).
+struct FieldGraph {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<long long> key;
+    ~FieldGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
 template <typename Real>
 void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConfig* c, Geometry<Real>& G,
                       RouteDev& R, const double* d_soc, DBuf<Real>& d_G, DBuf<double>& d_field_ext,
-                      cudaStream_t st, int64_t* launches, double* sweep_ms) {
+                      cudaStream_t st, int64_t* launches, double* sweep_ms, FieldGraph* fg = nullptr) {
     const int nv = c->n_v, nx = c->n_soc;
     const size_t lvl = (size_t)nv * nx;
     field_init_kernel<<<1, 256, 0, st>>>(d_soc, R.vaxes.p + (size_t)(n - 1) * nv, nv, nx, c->soc_target,
@@ -855,21 +864,43 @@ void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConf
     ECO_CUDA(cudaGetLastError());
     *launches += 2;
     const TileCfg tc = tile_cfg(G, 1, 1);
+    auto enqueue = [&](cudaStream_t qs) {
+        for (int s = n - 2; s >= 0; --s) {
+            StageArgs<Real> a = stage_args(G, s, R.vaxes.p + (size_t)s * nv, 1, tc);
+            a.J_next = d_G.p + (size_t)(s + 1) * lvl;
+            a.J_out = d_G.p + (size_t)s * lvl;
+            a.P_out = nullptr;
+            // always-green field: a light is an ordinary launch point (mpc.py:141-142)
+            a.src_kind = kinds[s] == ECO_NODE_SIGNAL ? ECO_NODE_PLAIN : kinds[s];
+            a.dwell = dwell;
+            a.j_inf = (Real)c->j_inf;
+            launch_stage<Real, 1>(a, tc, false, qs);
+        }
+    };
     EventTimer tm;
-    tm.start(st);
-    for (int s = n - 2; s >= 0; --s) {
-        StageArgs<Real> a = stage_args(G, s, R.vaxes.p + (size_t)s * nv, 1, tc);
-        a.J_next = d_G.p + (size_t)(s + 1) * lvl;
-        a.J_out = d_G.p + (size_t)s * lvl;
-        a.P_out = nullptr;
-        // always-green field: a light is an ordinary launch point (mpc.py:141-142)
-        a.src_kind = kinds[s] == ECO_NODE_SIGNAL ? ECO_NODE_PLAIN : kinds[s];
-        a.dwell = dwell;
-        a.j_inf = (Real)c->j_inf;
-        launch_stage<Real, 1>(a, tc, false, st);
-        ++*launches;
+    if (fg && st && env_int("ECO_GRAPH", 1) != 0) {
+        // the N-1 launches as one graph (captured once per geometry / buffers)
+        const std::vector<long long> key = {(long long)(size_t)G.act.p, (long long)(size_t)G.row.p,
+                                            (long long)(size_t)d_G.p, tc.slices, n};
+        if (!fg->exec || fg->key != key) {
+            if (fg->exec) { cudaGraphExecDestroy(fg->exec); fg->exec = nullptr; }
+            cudaGraph_t graph;
+            ECO_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            enqueue(st);
+            ECO_CUDA(cudaStreamEndCapture(st, &graph));
+            ECO_CUDA(cudaGraphInstantiate(&fg->exec, graph, 0));
+            cudaGraphDestroy(graph);
+            fg->key = key;
+        }
+        tm.start(st);
+        ECO_CUDA(cudaGraphLaunch(fg->exec, st));
+        tm.stop(st);
+    } else {
+        tm.start(st);
+        enqueue(st);
+        tm.stop(st);
     }
-    tm.stop(st);
+    *launches += n - 1;
     to_external_kernel<Real><<<grid_for((size_t)(n - 1) * lvl), 256, 0, st>>>(d_G.p, d_field_ext.p,
                                                                              (size_t)(n - 1) * lvl, c->j_inf);
     ECO_CUDA(cudaGetLastError());
@@ -972,6 +1003,7 @@ struct Session : SessionBase {
     // node), captured on first use and replayed: no per-kernel launch gaps
     cudaGraphExec_t gexec = nullptr;
     std::vector<long long> gkey;
+    FieldGraph fgraph;             // the terminal-field sweep, replayed per fit
 
     Session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
         cfg = *c;
@@ -1017,7 +1049,7 @@ struct Session : SessionBase {
         if (cfg.use_terminal_field) {
             if (field_in) field.upload(field_in, (size_t)n * lvl, st);
             else field_build_impl<Real>(kinds.data(), n, stop_dwell, &cfg, ctx.G, ctx.R, ctx.soc.p, field_int,
-                                        field, st, &launches, &sweep_ms);
+                                        field, st, &launches, &sweep_ms, &fgraph);
         }
         all.stop(st);
         if (field_out && cfg.use_terminal_field) field.download(field_out, (size_t)n * lvl, st);

@@ -1160,20 +1160,32 @@ field_stage_kernel(StageArgs<Real> a) {
     if (jx < nx) {
         const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
         const RowRec<Real>* rows = a.row + a.row_off[iv] + jx;
-        for (int k = slice; k < count; k += a.slices) {
-            const RowRec<Real> ro = rows[(size_t)k * nx];
-            if (ro.off < 0) continue;
-            const ActRec<Real> rc = acts[k];
-            const Real* b = a.J_next + ro.cell;
-            const int dv = (rc.meta & kRecDvh) ? nx : 0;     // next speed plane of G (v, soc)
-            const int dx = ro.wx > (Real)0 ? 1 : 0;
-            const Real lo = lerp(__ldg(b), __ldg(b + dv), rc.wv);                    // bilin2_abs K:335-337
-            const Real hi = lerp(__ldg(b + dx), __ldg(b + dv + dx), rc.wv);
-            const Real gn = lerp(lo, hi, ro.wx);
-            Real F;
-            if (hold) F = (Real)(a.c1d[(size_t)iv * a.U + k] + wait_cost) + gn;      // K:862
-            else F = rc.c1 + gn;
-            if (F < best) { best = F; bk = k; }
+        // kFU actions per round: their record loads are in flight together
+        constexpr int kFU = 4;
+        for (int k0 = slice; k0 < count; k0 += kFU * a.slices) {
+            RowRec<Real> ro[kFU];
+            ActRec<Real> rc[kFU];
+#pragma unroll
+            for (int q = 0; q < kFU; ++q) {
+                const int k = k0 + q * a.slices;
+                if (k < count) { ro[q] = rows[(size_t)k * nx]; rc[q] = acts[k]; }
+                else ro[q].off = -1;
+            }
+#pragma unroll
+            for (int q = 0; q < kFU; ++q) {
+                const int k = k0 + q * a.slices;
+                if (ro[q].off < 0) continue;
+                const Real* b = a.J_next + ro[q].cell;
+                const int dv = (rc[q].meta & kRecDvh) ? nx : 0;     // next speed plane of G (v, soc)
+                const int dx = ro[q].wx > (Real)0 ? 1 : 0;
+                const Real lo = lerp(__ldg(b), __ldg(b + dv), rc[q].wv);                 // bilin2_abs K:335-337
+                const Real hi = lerp(__ldg(b + dx), __ldg(b + dv + dx), rc[q].wv);
+                const Real gn = lerp(lo, hi, ro[q].wx);
+                Real F;
+                if (hold) F = (Real)(a.c1d[(size_t)iv * a.U + k] + wait_cost) + gn;   // K:862
+                else F = rc[q].c1 + gn;
+                if (F < best) { best = F; bk = k; }
+            }
         }
     }
     s_best[threadIdx.x] = best;
