@@ -522,16 +522,22 @@ struct HorizonInputs {
     DBuf<DevPlan> plans;
     DBuf<double> v, tdep, wait, te, tb, soc;
     DBuf<uint8_t> green, dep;
+    DBuf<int> flags;           // kStageAny* per stage
     void upload(const EcoPlant* p, const EcoProblem* pr, const EcoStepPlan* pl, int H, cudaStream_t st) {
         const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t;
         std::vector<DevPlan> hp(H);
         std::vector<double> hv((size_t)H * nv);
         std::vector<uint8_t> hgreen((size_t)H * nt), hdep((size_t)H * nt);
         std::vector<double> htdep((size_t)H * nt), hwait((size_t)H * nt);
+        std::vector<int> hflags(H, 0);
         for (int k = 0; k < H; ++k) {
             const EcoStepPlan& s = pl[k];
             if (!s.v_src || !s.arr_green || !s.dep_ok || !s.t_dep || !s.wait) throw ArgError{"null plan array"};
             hp[k] = dev_plan(s);
+            for (int z = 0; z < nt; ++z) {
+                if (s.arr_green[z] == 0) hflags[k] |= kStageAnyRed;
+                if (s.dep_ok[z] == 0 || s.wait[z] > 0.0) hflags[k] |= kStageAnyHold;
+            }
             std::memcpy(&hv[(size_t)k * nv], s.v_src, sizeof(double) * nv);
             std::memcpy(&hgreen[(size_t)k * nt], s.arr_green, nt);
             std::memcpy(&hdep[(size_t)k * nt], s.dep_ok, nt);
@@ -541,7 +547,8 @@ struct HorizonInputs {
         plant.ensure(1);
         plant.upload(p, 1, st);
         plans.ensure(H); v.ensure((size_t)H * nv); tdep.ensure((size_t)H * nt); wait.ensure((size_t)H * nt);
-        green.ensure((size_t)H * nt); dep.ensure((size_t)H * nt);
+        green.ensure((size_t)H * nt); dep.ensure((size_t)H * nt); flags.ensure(H);
+        flags.upload(hflags.data(), H, st);
         te.ensure(pr->n_te); tb.ensure(pr->n_tb); soc.ensure(nx);
         plans.upload(hp.data(), H, st);
         v.upload(hv.data(), hv.size(), st);
@@ -696,6 +703,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         a.dep_ok = d_dep.p + (size_t)k * nt;
         a.t_dep = d_tdep.p + (size_t)k * nt;
         a.wait = d_wait.p + (size_t)k * nt;
+        a.flags = in.flags.p + k;
         a.J_next = d_J.p + (size_t)(k + 1) * LV;
         a.J_next1 = a.J_next + LC;
         a.J_out = d_J.p + (size_t)k * LV;
@@ -992,6 +1000,7 @@ struct Session : SessionBase {
     DBuf<LoopState> state;
     DBuf<uint8_t> green, dep;
     DBuf<double> tdep, wait, tax;
+    DBuf<int> sflags;              // kStageAny* per stage of the current solve
     DBuf<Real> J;
     DBuf<int32_t> P;
     DBuf<EcoTrajRow> rows;
@@ -1022,6 +1031,7 @@ struct Session : SessionBase {
         state.alloc(1);
         green.alloc((size_t)(H + 1) * nt); dep.alloc((size_t)(H + 1) * nt);
         tdep.alloc((size_t)(H + 1) * nt); wait.alloc((size_t)(H + 1) * nt); tax.alloc(nt);
+        sflags.alloc(H);
         J.alloc((size_t)(H + 1) * level_stride(ns));
         P.alloc(ns);
         rows.alloc(n - 1);
@@ -1079,7 +1089,7 @@ struct Session : SessionBase {
         LoopState h0{};
         h0.x[0] = x0[0]; h0.x[1] = x0[1]; h0.x[2] = x0[2];
         EventTimer all;
-        Ladders lad{green.p, dep.p, tdep.p, wait.p, tax.p};
+        Ladders lad{green.p, dep.p, tdep.p, wait.p, tax.p, sflags.p};
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
@@ -1136,6 +1146,7 @@ struct Session : SessionBase {
                     a.status = &state.p->status;
                     a.live = count ? live.p : nullptr;
                     a.src_kind = kinds[s + k];
+                    a.flags = sflags.p + k;
                     a.t0_dev = tax.p;   // ladder origin depends on the device-resident clock
                     a.dtg = cfg.dt;
                     a.j_inf = (Real)cfg.j_inf;
@@ -1247,6 +1258,7 @@ struct Batch : BatchBase {
     DBuf<int32_t> s_d, h_d, P0_d;
     DBuf<double> t_d, tdep, wait, tax, J0_d;
     DBuf<uint8_t> green, dep;
+    DBuf<int> bflags;
     DBuf<Real> J;
     DBuf<unsigned long long> live;
     cudaStream_t st = 0;
@@ -1291,6 +1303,7 @@ struct Batch : BatchBase {
         s_d.alloc(B); h_d.alloc(B); t_d.alloc(B);
         green.alloc(B * (H + 1) * nt); dep.alloc(B * (H + 1) * nt);
         tdep.alloc(B * (H + 1) * nt); wait.alloc(B * (H + 1) * nt); tax.alloc(B * nt);
+        bflags.alloc(B * H);
         J.alloc(B * 2 * level_stride(ns));
         cap = B;
     }
@@ -1355,7 +1368,8 @@ struct Batch : BatchBase {
             const unsigned pblocks = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (ns + 255) / 256));
             batch_prepare_kernel<Real><<<dim3(pblocks, B), 256, 0, st>>>(
                 ctx.R.view, lc, sig_of_node.p, n_sig, tim.p, s_d.p, h_d.p, t_d.p, Hmax,
-                cfg.use_terminal_field ? field.p : nullptr, green.p, dep.p, tdep.p, wait.p, tax.p, J.p, LV, LC);
+                cfg.use_terminal_field ? field.p : nullptr, green.p, dep.p, tdep.p, wait.p, tax.p, J.p, LV, LC,
+                bflags.p);
             ECO_CUDA(cudaGetLastError());
             ++launches;
             BatchArgs<Real> ba{};
@@ -1368,6 +1382,7 @@ struct Batch : BatchBase {
             ba.Hmax = Hmax;
             ba.s = s_d.p; ba.h = h_d.p;
             ba.green = green.p; ba.dep_ok = dep.p; ba.t_dep = tdep.p; ba.wait = wait.p; ba.t_axis = tax.p;
+            ba.flags = bflags.p;
             ba.J = J.p; ba.LV = LV; ba.LC = LC;
             if (P0 && P0_d.n < (size_t)B * ns) P0_d.alloc((size_t)std::min(chunk, n_scen) * ns);
             ba.P0 = P0 ? P0_d.p : nullptr;
@@ -1598,6 +1613,7 @@ struct Slab : SlabBase {
         for (int k = H - 1; k >= 0; --k) {
             StageArgs<Real> a = stage_args(G, k, in.v.p + (size_t)k * nv, nt, tc);
             a.green = in.green.p + (size_t)k * nt;
+            a.flags = in.flags.p + k;
             a.dep_ok = in.dep.p + (size_t)k * nt;
             a.t_dep = in.tdep.p + (size_t)k * nt;
             a.wait = in.wait.p + (size_t)k * nt;

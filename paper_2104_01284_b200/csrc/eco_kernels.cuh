@@ -23,6 +23,10 @@ struct DevPlan {
     double cos_g, sin_g, v0d, dvd;
 };
 
+// Per-stage ladder summary bits (built with the ladders, read once per CTA)
+constexpr int kStageAnyRed = 1;            // some arrival sample of the destination is red
+constexpr int kStageAnyHold = 2;           // the source node holds a standstill (red wait / dwell / no departure)
+
 // ActRec::meta bits: zoff (bits 0..15, clamped to n_t) | flags
 constexpr uint32_t kRecZoff = 0xFFFFu;
 constexpr uint32_t kRecDzh = 1u << 16;     // wz > 0: time blend uses zlo+1 (K:513)
@@ -441,6 +445,7 @@ struct StageArgs {
     int count_max, band_cap;      // staging capacity: actions per plane, band elements
     int wide;                     // > 0: wide-row path, warps per row (n_t >= 128)
     int alias;                    // reduction buffers alias the staging region (TileSmem)
+    const int* flags;             // this stage's kStageAny* bits (nullable: derived from the ladders)
     Real* const* peer_base;       // C5 P2P exchange: level-0 base of each peer replica (device array)
     int npeer;
     size_t peer_off;              // this stage's level offset in a replica
@@ -607,18 +612,30 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     uint8_t* s_green = smem + L.green;
     Real* s_best = (Real*)(smem + L.red_best);
     int32_t* s_arg = (int32_t*)(smem + L.red_arg);
-    int red = 0, held = 0;
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-        const uint8_t g = a.green[i];
-        s_green[i] = g;
-        red |= (g == 0);
-        held |= (a.dep_ok[i] == 0) | (a.wait[i] > 0.0);
+    // any_red: any red arrival sample at all (plain / stop destinations:
+    // never).  any_hold: a standstill plane whose node never holds (no red
+    // wait, no stop dwell, departures always allowed) moves exactly like a
+    // moving one (K:528-533).  Precomputed per stage (flags) when available.
+    bool any_red, any_hold;
+    if (a.flags) {
+        const int fl = *a.flags;
+        any_red = (fl & kStageAnyRed) != 0;
+        any_hold = (fl & kStageAnyHold) != 0 && v == 0.0;
+        if (any_red) {
+            for (int i = threadIdx.x; i < nt; i += blockDim.x) s_green[i] = a.green[i];
+            __syncthreads();
+        }
+    } else {
+        int red = 0, held = 0;
+        for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+            const uint8_t g = a.green[i];
+            s_green[i] = g;
+            red |= (g == 0);
+            held |= (a.dep_ok[i] == 0) | (a.wait[i] > 0.0);
+        }
+        any_red = __syncthreads_or(red) != 0;
+        any_hold = __syncthreads_or(held) != 0 && v == 0.0;
     }
-    // any red arrival sample at all?  (plain / stop destinations: never)
-    const bool any_red = __syncthreads_or(red) != 0;
-    // a standstill plane whose node never holds (no red wait, no stop dwell,
-    // departures always allowed) moves exactly like a moving one (K:528-533)
-    const bool any_hold = __syncthreads_or(held) != 0 && v == 0.0;
 
     const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
     const RowRec<Real>* rows = a.row + tp->row_off + j0;       // + k * nx + r
@@ -1004,7 +1021,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                     zhi = zlo + ((rc.meta & kRecDzh) ? 1 : 0);
                     wz = rc.wz;
                 }
-                if ((rc.meta & kRecGated) && s_green[zlo] == 0) continue;
+                if (any_red && (rc.meta & kRecGated) && s_green[zlo] == 0) continue;
                 if (COUNT) ++nlive;
                 const Real* b = a.J_next + (ro.off - zoff);     // (ivlo, jxlo, t' = 0)
                 const int dv = (rc.meta & kRecDvh) ? plane : 0;
@@ -1067,7 +1084,8 @@ template <typename Real, bool COUNT, bool PEERS = false>
 __global__ void __launch_bounds__(512)
 bellman_stage_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
-    if (a.status && *a.status != 0) return;
+    // (a stopped closed loop (a.status) needs no early exit here: prepare and
+    // decide skip, so this stage's output is never read)
     extern __shared__ __align__(16) unsigned char smem[];
     stage_tile<Real, COUNT, false, PEERS>(a, blockIdx.x, smem);
 }
@@ -1079,7 +1097,6 @@ template <typename Real, bool COUNT, bool PEERS = false>
 __global__ void __launch_bounds__(256, ECO_WIDE_MINB)
 bellman_wide_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
-    if (a.status && *a.status != 0) return;
     extern __shared__ __align__(16) unsigned char smem[];
     stage_tile<Real, COUNT, true, PEERS>(a, blockIdx.x, smem);
 }
@@ -1103,6 +1120,7 @@ struct BatchArgs {
     const double* t_dep;
     const double* wait;
     const double* t_axis;         // [B][nt]
+    const int* flags;             // [B][Hmax] kStageAny* bits
     Real* J;                      // [B][2] levels of LV elements (copy 0 at +0, copy 1 at +LC)
     size_t LV, LC;
     int32_t* P0;                  // [B][nv*nx*nt] or nullptr
@@ -1128,6 +1146,7 @@ bellman_batch_kernel(BatchArgs<Real> ba) {
     a.t_dep = ba.t_dep + (lad + k) * a.nt;
     a.wait = ba.wait + (lad + k) * a.nt;
     a.t0_dev = ba.t_axis + (size_t)b * a.nt;
+    a.flags = ba.flags ? ba.flags + (size_t)b * ba.Hmax + k : nullptr;
     Real* Jb = ba.J + (size_t)b * 2 * ba.LV;
     a.J_next = Jb + ((k + 1) & 1) * ba.LV;
     a.J_next1 = a.J_next + ba.LC;

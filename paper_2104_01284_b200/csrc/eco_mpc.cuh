@@ -43,7 +43,25 @@ struct Ladders {                // [H+1][nt] per receding-horizon solve
     double* t_dep;
     double* wait;
     double* t_axis;             // [nt]
+    int* flags;                 // [H] kStageAny* of stage k (nullable)
 };
+
+// kStageAny* bits of stages 0..h-1 from ladders [h+1][nt] (stage k arrives at
+// node k + 1, departs node k); one block, after the ladders are complete.
+__device__ __forceinline__ void ladder_flags(const uint8_t* green, const uint8_t* dep, const double* wait, int nt,
+                                             int h, int* flags) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = w; k < h; k += nw) {
+        int red = 0, hold = 0;
+        for (int z = lane; z < nt; z += 32) {
+            red |= green[(size_t)(k + 1) * nt + z] == 0;
+            hold |= (dep[(size_t)k * nt + z] == 0) | (wait[(size_t)k * nt + z] > 0.0);
+        }
+        red = __any_sync(0xffffffffu, red);
+        hold = __any_sync(0xffffffffu, hold);
+        if (lane == 0) flags[k] = (red ? kStageAnyRed : 0) | (hold ? kStageAnyHold : 0);
+    }
+}
 
 struct LoopCfg {
     int nv, nx, nt, nte, ntb, U, H, teleport, use_field;
@@ -122,6 +140,10 @@ __global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, i
             const int k = i / nt, z = i - k * nt;
             node_ladder(r, s + k, tax, nt, c.teleport, lad.green + k * nt, lad.dep_ok + k * nt,
                         lad.t_dep + k * nt, lad.wait + k * nt, z);
+        }
+        if (lad.flags) {
+            __syncthreads();
+            ladder_flags(lad.green, lad.dep_ok, lad.wait, nt, h, lad.flags);
         }
     }
     const int ncell = c.nv * c.nx;
@@ -340,23 +362,29 @@ __global__ void batch_prepare_kernel(DevRoute r, LoopCfg c, const int32_t* __res
                                      const EcoSignalTiming* __restrict__ timings, const int32_t* __restrict__ s_arr,
                                      const int32_t* __restrict__ h_arr, const double* __restrict__ t_start, int Hmax,
                                      const double* __restrict__ field, uint8_t* green, uint8_t* dep, double* tdep,
-                                     double* wait, double* t_axis, Real* J, size_t LV, size_t LC) {
+                                     double* wait, double* t_axis, Real* J, size_t LV, size_t LC, int* flags) {
     const int b = blockIdx.y;
     const int s = s_arr[b], h = h_arr[b];
     const int nt = c.nt;
     const double t0 = c.dt * floor(t_start[b] / c.dt);
     double* tax = t_axis + (size_t)b * nt;
     const size_t lad = (size_t)b * (Hmax + 1) * nt;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (h + 1) * nt; i += gridDim.x * blockDim.x) {
-        const int k = i / nt, z = i - k * nt;
-        const int node = s + k;
-        const double tz = t0 + c.dt * (double)z;
-        if (k == 0) tax[z] = tz;
-        const int si = sig_of_node[node];
-        const EcoSignalTiming* tm = si >= 0 ? timings + (size_t)b * n_sig + si : nullptr;
-        ladder_entry(r.kinds[node], tm ? tm->cycle : 1.0, tm ? tm->offset : 0.0, tm ? &tm->win[0][0] : nullptr,
-                     tm ? tm->nwin : 0, r.stop_dwell, tz, c.teleport, green + lad, dep + lad, tdep + lad,
-                     wait + lad, i);
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < (h + 1) * nt; i += blockDim.x) {
+            const int k = i / nt, z = i - k * nt;
+            const int node = s + k;
+            const double tz = t0 + c.dt * (double)z;
+            if (k == 0) tax[z] = tz;
+            const int si = sig_of_node[node];
+            const EcoSignalTiming* tm = si >= 0 ? timings + (size_t)b * n_sig + si : nullptr;
+            ladder_entry(r.kinds[node], tm ? tm->cycle : 1.0, tm ? tm->offset : 0.0, tm ? &tm->win[0][0] : nullptr,
+                         tm ? tm->nwin : 0, r.stop_dwell, tz, c.teleport, green + lad, dep + lad, tdep + lad,
+                         wait + lad, i);
+        }
+        if (flags) {
+            __syncthreads();
+            ladder_flags(green + lad, dep + lad, wait + lad, nt, h, flags + (size_t)b * Hmax);
+        }
     }
     const int ncell = c.nv * c.nx;
     const int total = ncell * nt;
