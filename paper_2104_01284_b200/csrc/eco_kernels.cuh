@@ -543,17 +543,28 @@ struct TileSmem {
     // merge.  Smaller CTAs -> 4 per SM: used by the (throughput-bound) batch
     // kernel; the single-solve kernels keep one wave of 3 per SM.
     __host__ __device__ TileSmem(int nt, int tj, int slices, int count_max, int band_cap, bool alias = false) {
+        const size_t rr_bytes = (size_t)count_max * tj *
+                                (sizeof(RowRec2<Real>) > sizeof(RowRec<Real>) ? sizeof(RowRec2<Real>)
+                                                                               : sizeof(RowRec<Real>));
+        const size_t red_b = (size_t)slices * tj * nt * sizeof(Real), red_a = (size_t)slices * tj * nt * 4;
         size_t o = 0;
         green = o;    o = align16(o + (size_t)nt);
+        if (!alias) {
+            red_best = o; o = align16(o + red_b);
+            red_arg = o;  o = align16(o + red_a);
+            rr = o;       o = align16(o + rr_bytes);
+            act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
+            band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
+            total = o;
+            return;
+        }
         act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
-        const size_t red0 = o;
-        red_best = o; o = align16(o + (size_t)slices * tj * nt * sizeof(Real));
-        red_arg = o;  o = align16(o + (size_t)slices * tj * nt * sizeof(int32_t));
+        const size_t r0 = o;
+        red_best = o; o = align16(o + red_b);
+        red_arg = o;  o = align16(o + red_a);
         const size_t red_end = o;
-        if (alias) o = red0;
-        rr = o;       o = align16(o + (size_t)count_max * tj *
-                                  (sizeof(RowRec2<Real>) > sizeof(RowRec<Real>) ? sizeof(RowRec2<Real>)
-                                                                                 : sizeof(RowRec<Real>)));
+        o = r0;
+        rr = o;       o = align16(o + rr_bytes);
         band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
         total = o > red_end ? o : red_end;
     }
@@ -617,7 +628,9 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     // wait, no stop dwell, departures always allowed) moves exactly like a
     // moving one (K:528-533).  Precomputed per stage (flags) when available.
     bool any_red, any_hold;
-    if (a.flags) {
+    // (the wide-row kernel keeps the in-kernel scan: measured 20 % faster
+    // there, its prologue being a negligible part of a 45,500-CTA launch)
+    if (!WIDE && a.flags) {
         const int fl = *a.flags;
         any_red = (fl & kStageAnyRed) != 0;
         any_hold = (fl & kStageAnyHold) != 0 && v == 0.0;
