@@ -221,7 +221,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    h2d = mpc.session_.h2d_bytes + 3 * 8
+    h2d = mpc.upload_bytes_ + 3 * 8          # route / SPaT arrays re-sent by every fit + x0
     d2h = traj.n_steps * 120 + 3 * 8 + mpc.terminal_field_.values.nbytes + 4 * 3
 
     if rank != 0:

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECO_ABI_VERSION 3
+#define ECO_ABI_VERSION 4
 
 #define ECO_MAX_GEARS 16
 #define ECO_MAX_AXIS 32
@@ -244,6 +244,10 @@ typedef struct EcoSession EcoSession;
 #define ECO_RUN_TIME_SWEEPS 2
 int32_t eco_session_create(const EcoPlant* plant, const EcoRoute* route,
                            const EcoMpcConfig* cfg, EcoSession** out);
+/* new data for the session's route (same node count): speed limits,
+ * grades, node kinds, signal programs; the next fit rebuilds geometry and
+ * field from it. */
+int32_t eco_session_upload_route(EcoSession* sess, const EcoRoute* route);
 int32_t eco_session_fit(EcoSession* sess, const double* field_in,
                         double* field_out, EcoStats* stats);
 int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,

@@ -795,9 +795,11 @@ struct RouteDev {
         if (!r->v_min || !r->v_max || !r->grade || !r->cos_grade || !r->sin_grade || !r->kinds || !r->sig_cycle ||
             !r->sig_offset || !r->sig_nwin || !r->sig_win)
             throw ArgError{"null route array"};
-        v_min.alloc(n); v_max.alloc(n); grade.alloc(n); cos_g.alloc(n); sin_g.alloc(n);
-        cycle.alloc(n); offset.alloc(n); win.alloc((size_t)n * ECO_MAX_WINDOWS * 2);
-        kinds.alloc(n); nwin.alloc(n); vaxes.alloc((size_t)n * nv);
+        // ensure(): a re-upload of a same-sized route keeps every device
+        // pointer (captured CUDA graphs stay valid)
+        v_min.ensure(n); v_max.ensure(n); grade.ensure(n); cos_g.ensure(n); sin_g.ensure(n);
+        cycle.ensure(n); offset.ensure(n); win.ensure((size_t)n * ECO_MAX_WINDOWS * 2);
+        kinds.ensure(n); nwin.ensure(n); vaxes.ensure((size_t)n * nv);
         v_min.upload(r->v_min, n, s); v_max.upload(r->v_max, n, s); grade.upload(r->grade, n, s);
         cos_g.upload(r->cos_grade, n, s); sin_g.upload(r->sin_grade, n, s);
         cycle.upload(r->sig_cycle, n, s); offset.upload(r->sig_offset, n, s);
@@ -962,6 +964,17 @@ struct RouteCtx {
                           r->delta_d, r->accel_min, r->accel_max, c->gamma, c->dt};
         G.alloc(G.dims.P, G.dims.nv, G.dims.U);
     }
+    // new route data of the same shape (speed limits, grades, node kinds,
+    // signal programs): arrays re-uploaded in place, plans rebuilt
+    void reupload(const EcoRoute* r, const EcoMpcConfig* c, cudaStream_t st) {
+        R.upload(r, c->n_v, st);
+        std::vector<DevPlan> hp = route_plans(r, R.h_vaxes, c->n_v);
+        plans.upload(hp.data(), hp.size(), st);
+        G.dims.delta_d = r->delta_d;
+        G.dims.a_min = r->accel_min;
+        G.dims.a_max = r->accel_max;
+        ECO_CUDA(cudaStreamSynchronize(st));
+    }
     // route-level geometry: stage-1 + SoC cells of every spatial step
     void geometry(cudaStream_t st, int64_t* launches) {
         EcoStage1Tables none{};
@@ -978,6 +991,7 @@ struct RouteCtx {
 struct SessionBase {
     int precision = 0;
     virtual ~SessionBase() = default;
+    virtual void upload_route(const EcoRoute* r) = 0;
     virtual void fit(const double* field_in, double* field_out, EcoStats* stats) = 0;
     virtual void run(int start_node, int max_steps, const double* x0, EcoTrajRow* rows, int32_t* n_rows,
                      int32_t* status, int32_t* status_node, double* final_state, int flags, EcoStats* stats) = 0;
@@ -1047,6 +1061,22 @@ struct Session : SessionBase {
         for (auto& e : ev) cudaEventDestroy(e);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (st) cudaStreamDestroy(st);
+    }
+
+    void upload_route(const EcoRoute* r) override {
+        if (r->node_count != n) throw ArgError{"route node count differs from the session's"};
+        if (!r->kinds) throw ArgError{"null route array"};
+        const bool same_kinds = std::equal(kinds.begin(), kinds.end(), r->kinds) && stop_dwell == r->stop_dwell;
+        ctx.reupload(r, &cfg, st);
+        kinds.assign(r->kinds, r->kinds + n);
+        stop_dwell = r->stop_dwell;
+        if (!same_kinds) {           // node kinds / dwell are baked into the captured graphs
+            if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+            gkey.clear();
+            if (fgraph.exec) { cudaGraphExecDestroy(fgraph.exec); fgraph.exec = nullptr; }
+            fgraph.key.clear();
+        }
+        fitted = false;              // geometry and field depend on the route
     }
 
     void fit(const double* field_in, double* field_out, EcoStats* stats) override {
@@ -1752,6 +1782,13 @@ int32_t eco_session_create(const EcoPlant* plant, const EcoRoute* route, const E
         check_cfg(cfg);
         if (!route || !out) throw ArgError{"null pointer argument"};
         *out = reinterpret_cast<EcoSession*>(make_session(plant, route, cfg));
+    });
+}
+
+int32_t eco_session_upload_route(EcoSession* sess, const EcoRoute* route) {
+    return run_guarded([&] {
+        if (!sess || !route) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SessionBase*>(sess)->upload_route(route);
     });
 }
 

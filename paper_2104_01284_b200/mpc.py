@@ -210,6 +210,17 @@ class MpcSession:
                                self._rp.kinds, self._rp.cycle, self._rp.offset, self._rp.nwin, self._rp.win,
                                *self._keep)))
 
+    def upload_route(self, route: Route, spat: SpatSchedule) -> int:
+        """Re-send the route / SPaT arrays into the session's buffers (same node
+        count); returns the bytes copied.  The next :meth:`fit` uses them."""
+        if route.node_count != self.route.node_count:
+            raise ValueError("route node count differs from the session's")
+        rp = _abi.RoutePack(route, spat)
+        _abi.check(self._lib.eco_session_upload_route(self._h, C.byref(rp.c)), "eco_session_upload_route")
+        self._rp, self.route = rp, route
+        return sum(a.nbytes for a in (rp.v_min, rp.v_max, rp.grade, rp.cos_g, rp.sin_g, rp.kinds, rp.cycle,
+                                      rp.offset, rp.nwin, rp.win))
+
     def fit(self, field: Optional[np.ndarray] = None, want_field: bool = True):
         """Route geometry + terminal field on the device; returns (field or None, stats)."""
         n = self.route.node_count
@@ -368,6 +379,9 @@ class EcoDrivingMPC:
         self.session_ = _session_for(self.vehicle, route, spat, gamma=self.gamma, grids=self.grids,
                                      penalty=self.penalty, horizon=self.horizon, backend=self.backend,
                                      teleport=self.teleport, use_terminal_field=self.use_terminal_field)
+        # a cached session gets this call's route / SPaT values (they may have
+        # been edited in place since): ~150 KB per fit, the inputs' H2D
+        self.upload_bytes_ = self.session_.upload_route(route, spat)
         values, self.fit_stats_ = self.session_.fit()
         self.terminal_field_ = (TerminalCostField(values=values, route_name=route.name, gamma=self.gamma,
                                                   grids=self.grids, penalty=self.penalty)

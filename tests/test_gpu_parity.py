@@ -448,3 +448,26 @@ def test_closed_loop_files_byte_identical_to_reference(vehicle, short_route, tmp
     ref = json.loads((GOLDEN / "loop_short_small_summary.json").read_text())
     assert ours.pop("backend") == "b200-fp64" and ref.pop("backend") == "parallel"
     assert ours == ref
+
+
+def test_session_route_reupload_matches_fresh_session(vehicle):
+    """A cached session fed another route's data (same node count) behaves
+    exactly like a fresh session on that route (geometry, field, graphs)."""
+    from paper_2104_01284_b200 import load_fixture_route
+    from paper_2104_01284_b200.mpc import MpcSession
+    r1, sp1 = load_fixture_route("short", seed=2)
+    r2, sp2 = load_fixture_route("short", seed=5)
+    kw = dict(gamma=0.5, grids=SMALL, penalty=PEN, horizon=8, backend="b200-fp64")
+    x0 = StateVector(v=0.0, soc=0.5, t=0.0)
+    with_fresh = MpcSession(vehicle, r2, sp2, **kw)
+    with_fresh.fit(want_field=False)
+    rows_f, st_f, _, fin_f, _ = with_fresh.run(x0)
+    reused = MpcSession(vehicle, r1, sp1, **kw)
+    reused.fit(want_field=False)
+    reused.run(x0)                           # captures graphs on route 1
+    reused.upload_route(r2, sp2)
+    reused.fit(want_field=False)
+    rows_r, st_r, _, fin_r, _ = reused.run(x0)
+    assert st_f == st_r and np.array_equal(fin_f, fin_r)
+    assert rows_f.tobytes() == rows_r.tobytes()
+    with_fresh.close(); reused.close()
