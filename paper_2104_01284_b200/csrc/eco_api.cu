@@ -1639,6 +1639,15 @@ struct Slab : SlabBase {
         ECO_CUDA(cudaGetLastError());
         ++launches;
         const TileCfg tc = tile_cfg(G, nt, 0);
+        // P2P: no rank may store into a peer's levels while that peer still
+        // reads its previous solve's tables (output conversion, D2H)
+        if (exchange == ECO_XCHG_P2P && nranks > 1) {
+            ++barriers;
+            slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
+                                                  (unsigned)(barriers * nranks), err.p);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
+        }
         sweep.start(st);
         for (int k = H - 1; k >= 0; --k) {
             StageArgs<Real> a = stage_args(G, k, in.v.p + (size_t)k * nv, nt, tc);
