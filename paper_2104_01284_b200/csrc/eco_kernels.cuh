@@ -844,10 +844,14 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 // pointers in registers for the others' immediate offsets)
                 const int mlive = min(kMW, ((zl + 1 - zs) >> 6) + 1);
                 PR col[kMW];
+#ifndef ECO_WIDE_FULL_FAST
+#define ECO_WIDE_FULL_FAST 1
+#endif
+                if (ECO_WIDE_FULL_FAST && mlive == kMW) {
+                    // every chunk live (the common case of a warp's first
+                    // segment): unpredicated loads at immediate offsets
 #pragma unroll
-                for (int m = 0; m < kMW; ++m) {
-                    col[m] = PR{(Real)INFINITY, (Real)INFINITY};
-                    if (m == 0 || m < mlive) {
+                    for (int m = 0; m < kMW; ++m) {
                         const V2 t00 = __ldg(reinterpret_cast<const V2*>(b00 + 64 * m));
                         const V2 t10 = __ldg(reinterpret_cast<const V2*>(b10 + 64 * m));
                         const V2 t01 = __ldg(reinterpret_cast<const V2*>(b01 + 64 * m));
@@ -855,6 +859,20 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                         const PR lo = p_lerp(PR{t00.x, t00.y}, PR{t10.x, t10.y}, rc.wv);   // v inside (K:335-337)
                         const PR hi = p_lerp(PR{t01.x, t01.y}, PR{t11.x, t11.y}, rc.wv);
                         col[m] = p_lerp(lo, hi, ro.wx);                                  // then soc
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) {
+                        col[m] = PR{(Real)INFINITY, (Real)INFINITY};
+                        if (m == 0 || m < mlive) {
+                            const V2 t00 = __ldg(reinterpret_cast<const V2*>(b00 + 64 * m));
+                            const V2 t10 = __ldg(reinterpret_cast<const V2*>(b10 + 64 * m));
+                            const V2 t01 = __ldg(reinterpret_cast<const V2*>(b01 + 64 * m));
+                            const V2 t11 = __ldg(reinterpret_cast<const V2*>(b11 + 64 * m));
+                            const PR lo = p_lerp(PR{t00.x, t00.y}, PR{t10.x, t10.y}, rc.wv);
+                            const PR hi = p_lerp(PR{t01.x, t01.y}, PR{t11.x, t11.y}, rc.wv);
+                            col[m] = p_lerp(lo, hi, ro.wx);
+                        }
                     }
                 }
                 PR F[kMW];
@@ -889,6 +907,18 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                         if (COUNT) nlive += ok0 + ok1;
                         const bool u0 = ok0 && F[m].x < best[2 * m];
                         const bool u1 = ok1 && F[m].y < best[2 * m + 1];
+                        best[2 * m] = u0 ? F[m].x : best[2 * m];
+                        bk[2 * m] = u0 ? k : bk[2 * m];
+                        best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
+                        bk[2 * m + 1] = u1 ? k : bk[2 * m + 1];
+                    }
+                } else if (zl >= zs + 64 * kMW - 1) {
+                    // every state of the warp's range is live: no masks
+#pragma unroll
+                    for (int m = 0; m < kMW; ++m) {
+                        if (COUNT) nlive += 2;
+                        const bool u0 = F[m].x < best[2 * m];
+                        const bool u1 = F[m].y < best[2 * m + 1];
                         best[2 * m] = u0 ? F[m].x : best[2 * m];
                         bk[2 * m] = u0 ? k : bk[2 * m];
                         best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
