@@ -4,7 +4,9 @@ Drop-in for the reference package's DP path (``ecodrive.dp`` / ``ecodrive.mpc``)
 same types and entry points, executed by hand-written sm_100a CUDA kernels
 behind the C ABI in ``include/eco_b200.h``.  ``plugin.install()`` registers the
 ``"b200"`` / ``"b200-fp64"`` backend names inside an importable reference
-package.
+package.  Beyond the reference's single-solve / closed-loop API:
+``BatchSolver`` (many scenarios on one road, C4) and ``SlabSolver`` (one grid
+split into speed-plane slabs across GPUs, C5).
 """
 
 from .dp import (BACKENDS, CostToGoTable, GridSpec, PenaltyConfig, PolicyTable, SolveContext, SolveResult,
@@ -17,5 +19,8 @@ from .mpc import (ClosedLoopTrajectory, ControlDecision, EcoDrivingMPC, Terminal
                   build_terminal_cost, field_value, mpc_step, simulate_closed_loop)
 from .plant import ActionVector, StateVector, Vehicle
 from .route import Route, SignalTiming, SpatSchedule, load_route, next_green_start, phase_at
+from .batch import BatchResult, BatchSolver, solve_batch
+from .slab import SlabResult, SlabSolver, gather_policies, make_partition
+from .io import read_trajectory_csv, summarize, write_summary_json, write_timing_csv, write_trajectory_csv
 
 __version__ = "0.1.0"
