@@ -471,3 +471,25 @@ def test_session_route_reupload_matches_fresh_session(vehicle):
     assert st_f == st_r and np.array_equal(fin_f, fin_r)
     assert rows_f.tobytes() == rows_r.tobytes()
     with_fresh.close(); reused.close()
+
+
+@pytest.mark.parametrize("nt", [128, 129, 130, 192, 256, 258, 322, 512])
+def test_wide_row_path_vs_oracle(vehicle, urban_route, nt):
+    """Long ladders take the wide-row kernel: odd chunk counts, partial last
+    chunks, ranges that end exactly on / one past a warp segment; fp64
+    bitwise against the oracle, fp32 within tolerance (incl. the signal at
+    node 80 inside the horizon: red gates, standstill relocation)."""
+    route, spat = urban_route
+    grids = GridSpec(n_v=7, n_soc=5, n_t=nt, dt=0.25)
+    for s, t in [(62, 31.0), (76, 5.5)]:
+        ctx = build_context(vehicle, route, spat, s, t, grids=grids, penalty=PEN, gamma=0.5, horizon=6)
+        J, P = O.solve_context(ctx)
+        r64 = solve_horizon(ctx, backend="b200-fp64")
+        for k in range(ctx.horizon):
+            assert np.array_equal(r64.tables[k].values, J[k]), (nt, s, k)
+            assert np.array_equal(r64.policies[k].values, P[k]), (nt, s, k)
+        r32 = solve_horizon(ctx, backend="b200")
+        J32 = np.stack([x.values for x in r32.tables[:-1]])
+        P32 = np.stack([x.values for x in r32.policies])
+        mask, p999, mx, pol = fp32_agreement(J32, P32, np.stack(J[:-1]), np.stack(P))
+        assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (nt, s, mask, p999, mx, pol)
