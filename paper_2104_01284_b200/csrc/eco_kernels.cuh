@@ -1097,17 +1097,36 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         dbg[4] = smid() | ((unsigned long long)((fast ? 1 : 0) + (nseg >= 0 ? 2 : 0)) << 16);
         dbg[5] = (unsigned long long)count * tja;
     }
-    // ---- merge slices: lexicographic (F, k); k ascends with the flat index
+    // ---- merge slices: lexicographic (F, k); k ascends with the flat index.
+    //      Two threads per state (adjacent lanes) take half the slices each
+    //      when the block has room; one shuffle joins them.
     const int32_t* u = a.u + (size_t)iv * a.U;
-    for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
-        Real best = s_best[f];
-        int bk = s_arg[f];
-        for (int s = 1; s < a.slices; ++s) {
-            const int k2 = s_arg[s * tj_nt + f];
-            if (k2 < 0) continue;
-            const Real b2 = s_best[s * tj_nt + f];
-            if (bk < 0 || b2 < best || (b2 == best && k2 < bk)) { best = b2; bk = k2; }
+    const bool pair = a.slices >= 4 && 2 * tstates <= (int)blockDim.x;
+    const int f_lim = pair ? 2 * tstates : tstates;
+    const int f_rnd = (f_lim + 31) & ~31;                 // whole warps take part in the shuffle
+    for (int t = threadIdx.x; t < f_rnd; t += blockDim.x) {
+        const int f = pair ? (t >> 1) : t;
+        const int half = pair ? (t & 1) : 0;
+        const bool live = t < f_lim;
+        const int s0 = pair ? half * ((a.slices + 1) >> 1) : 0;
+        const int s1 = pair ? (half ? a.slices : (a.slices + 1) >> 1) : a.slices;
+        Real best = (Real)INFINITY;
+        int bk = -1;
+        if (live) {
+            for (int s = s0; s < s1; ++s) {
+                const int k2 = s_arg[s * tj_nt + f];
+                if (k2 < 0) continue;
+                const Real b2 = s_best[s * tj_nt + f];
+                if (bk < 0 || b2 < best || (b2 == best && k2 < bk)) { best = b2; bk = k2; }
+            }
         }
+        if (pair) {
+            const Real b2 = __shfl_xor_sync(0xffffffffu, best, 1);
+            const int k2 = __shfl_xor_sync(0xffffffffu, bk, 1);
+            if (k2 >= 0 && (bk < 0 || b2 < best || (b2 == best && k2 < bk))) { best = b2; bk = k2; }
+            if (half) continue;
+        }
+        if (!live) continue;
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
         if (obase + f > 0) a.J_out1[obase + f - 1] = val;
