@@ -493,3 +493,20 @@ def test_wide_row_path_vs_oracle(vehicle, urban_route, nt):
         P32 = np.stack([x.values for x in r32.policies])
         mask, p999, mx, pol = fp32_agreement(J32, P32, np.stack(J[:-1]), np.stack(P))
         assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (nt, s, mask, p999, mx, pol)
+
+
+@pytest.mark.slow
+def test_c4_full_batch_fp32_vs_fp64(vehicle):
+    """All 4096 C4 scenarios: the fp32 start-node tables against the fp64
+    build (bitwise to the reference on the golden scenarios)."""
+    from paper_2104_01284_b200 import _abi
+    from paper_2104_01284_b200.batch import BatchSolver
+    routes, sched = _c4_scenarios(4096)
+    tim = _abi.signal_timings(routes[0][0], [sp for _, sp in routes])
+    kw = dict(grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20)
+    with BatchSolver(vehicle, routes[0][0], backend="b200-fp64", **kw) as b:
+        r64 = b.solve(None, sched, timings=tim)
+    with BatchSolver(vehicle, routes[0][0], backend="b200", **kw) as b:
+        r32 = b.solve(None, sched, timings=tim)
+    mask, p999, mx, pol = fp32_agreement(r32.J0, r32.P0, r64.J0, r64.P0)
+    assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (mask, p999, mx, pol)
