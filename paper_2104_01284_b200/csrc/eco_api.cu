@@ -298,9 +298,11 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode, bool alias = false) 
         // threads per action slice: one per kZP ladder states of the tile (a
         // warp may hold two slices); the per-state path strides over states
         const int per_row = (nt % 2 == 0) ? upr : nt;
-        t.S = std::min(512, t.tj * per_row);
+        t.S = std::min(256, t.tj * per_row);
+        if (nt % 2 == 0 && t.tj * upr > 256) throw ArgError{"stage tile too tall (lower ECO_TILE_TJ)"};
         const int sl_default = G.slices_pref > 0 ? G.slices_pref : std::max(1, 256 / t.S);
-        t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", sl_default), 512 / t.S));
+        // <= 256 threads: the single-solve stage kernel is built for 256-thread blocks
+        t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", sl_default), std::max(1, 256 / t.S)));
         t.count_max = std::max(1, G.h_gmax[0]);
         t.band_cap = G.band_cap;
         t.alias = alias ? 1 : 0;

@@ -1142,8 +1142,11 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
 
 // PEERS: the C5 P2P exchange variant (epilogue stores into peer replicas);
 // a separate instantiation keeps the plain kernels' code unchanged.
+#ifndef ECO_STAGE_MINB
+#define ECO_STAGE_MINB 3
+#endif
 template <typename Real, bool COUNT, bool PEERS = false>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(256, ECO_STAGE_MINB)
 bellman_stage_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     // (a stopped closed loop (a.status) needs no early exit here: prepare and
