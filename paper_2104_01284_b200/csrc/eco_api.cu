@@ -1287,8 +1287,10 @@ struct Batch : BatchBase {
     bool fitted = false;
     size_t cap = 0;                       // scenarios the per-chunk buffers hold
     DBuf<EcoSignalTiming> tim;
-    DBuf<int32_t> s_d, h_d, P0_d;
-    DBuf<double> t_d, tdep, wait, tax, J0_d;
+    DBuf<int32_t> s_d, h_d, P0_d[2];
+    DBuf<double> t_d, tdep, wait, tax, J0_d[2];
+    cudaStream_t st_out = 0;       // D2H of chunk c overlaps the compute of chunk c + 1
+    cudaEvent_t ev_out[2]{};
     DBuf<uint8_t> green, dep;
     DBuf<int> bflags;
     DBuf<Real> J;
@@ -1323,8 +1325,12 @@ struct Batch : BatchBase {
         live.alloc(1);
         ECO_CUDA(cudaStreamSynchronize(st));
         ECO_CUDA(cudaStreamCreate(&st));
+        ECO_CUDA(cudaStreamCreateWithFlags(&st_out, cudaStreamNonBlocking));
+        for (auto& e : ev_out) ECO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     ~Batch() override {
+        for (auto& e : ev_out) if (e) cudaEventDestroy(e);
+        if (st_out) cudaStreamDestroy(st_out);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -1369,7 +1375,23 @@ struct Batch : BatchBase {
             fit_ms = ft.ms();
             fitted = true;
         }
-        const int chunk = std::max(1, std::min(env_int("ECO_BATCH_CHUNK", 4096), 65535));
+        const bool outs = J0 || P0;
+        // with host outputs, smaller chunks let chunk c's D2H overlap chunk c + 1
+        const int chunk = std::max(1, std::min(outs ? env_int("ECO_BATCH_OUT_CHUNK", 1024)
+                                                    : env_int("ECO_BATCH_CHUNK", 4096), 65535));
+        int pending = -1;                 // chunk whose outputs still wait for their D2H
+        int pend_c0 = 0, pend_B = 0;
+        auto drain = [&]() {
+            if (pending < 0) return;
+            const int b = pending & 1;
+            ECO_CUDA(cudaStreamWaitEvent(st_out, ev_out[b], 0));
+            if (J0) ECO_CUDA(cudaMemcpyAsync(J0 + (size_t)pend_c0 * ns, J0_d[b].p, (size_t)pend_B * ns * sizeof(double),
+                                             cudaMemcpyDeviceToHost, st_out));
+            if (P0) ECO_CUDA(cudaMemcpyAsync(P0 + (size_t)pend_c0 * ns, P0_d[b].p, (size_t)pend_B * ns * sizeof(int32_t),
+                                             cudaMemcpyDeviceToHost, st_out));
+            ECO_CUDA(cudaStreamSynchronize(st_out));
+            pending = -1;
+        };
         const TileCfg tc = tile_cfg(ctx.G, nt, 0, env_int("ECO_BATCH_ALIAS", 1) != 0);
         const size_t LV = level_stride(ns), LC = level_copy(ns);
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
@@ -1380,8 +1402,9 @@ struct Batch : BatchBase {
         int64_t stages = 0;
         unsigned long long nlive = 0;
         if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
-        for (int c0 = 0; c0 < n_scen; c0 += chunk) {
+        for (int c0 = 0, ci = 0; c0 < n_scen; c0 += chunk, ++ci) {
             const int B = std::min(chunk, n_scen - c0);
+            const int ob = ci & 1;
             reserve((size_t)std::min(chunk, n_scen), H, ns);
             std::vector<int32_t> hh(B);
             int Hmax = 0;
@@ -1416,8 +1439,8 @@ struct Batch : BatchBase {
             ba.green = green.p; ba.dep_ok = dep.p; ba.t_dep = tdep.p; ba.wait = wait.p; ba.t_axis = tax.p;
             ba.flags = bflags.p;
             ba.J = J.p; ba.LV = LV; ba.LC = LC;
-            if (P0 && P0_d.n < (size_t)B * ns) P0_d.alloc((size_t)std::min(chunk, n_scen) * ns);
-            ba.P0 = P0 ? P0_d.p : nullptr;
+            if (P0 && P0_d[ob].n < (size_t)B * ns) P0_d[ob].alloc((size_t)std::min(chunk, n_scen) * ns);
+            ba.P0 = P0 ? P0_d[ob].p : nullptr;
             sw.start(st);
             for (int k = Hmax - 1; k >= 0; --k) {
                 ba.k = k;
@@ -1436,19 +1459,21 @@ struct Batch : BatchBase {
             }
             sw.stop(st);
             if (J0) {
-                if (J0_d.n < (size_t)B * ns) J0_d.alloc((size_t)std::min(chunk, n_scen) * ns);
-                to_external_strided_kernel<Real><<<grid_for((size_t)B * ns), 256, 0, st>>>(J.p, J0_d.p, ns, B, 2 * LV,
-                                                                                          cfg.j_inf);
+                if (J0_d[ob].n < (size_t)B * ns) J0_d[ob].alloc((size_t)std::min(chunk, n_scen) * ns);
+                to_external_strided_kernel<Real><<<grid_for((size_t)B * ns), 256, 0, st>>>(J.p, J0_d[ob].p, ns, B,
+                                                                                          2 * LV, cfg.j_inf);
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
             }
             all.stop(st);
-            if (J0) J0_d.download(J0 + (size_t)c0 * ns, (size_t)B * ns, st);
-            if (P0) P0_d.download(P0 + (size_t)c0 * ns, (size_t)B * ns, st);
-            ECO_CUDA(cudaStreamSynchronize(st));
+            if (outs) ECO_CUDA(cudaEventRecord(ev_out[ob], st));
+            // previous chunk's D2H (blocks this thread) while this chunk computes
+            drain();
+            if (outs) { pending = ci; pend_c0 = c0; pend_B = B; }
             sweep_ms += sw.ms();
             all_ms += all.ms();
         }
+        drain();
         if (count) {
             ECO_CUDA(cudaMemcpyAsync(&nlive, live.p, sizeof nlive, cudaMemcpyDeviceToHost, st));
             ECO_CUDA(cudaStreamSynchronize(st));
