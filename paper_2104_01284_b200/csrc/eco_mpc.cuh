@@ -246,6 +246,9 @@ mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, Loo
     const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
     double bestf = 0.0;
     int bestu = -1;
+    // the winner's predicted state and plant-step outputs (v', soc', t',
+    // dt_move, fuel rate, accel) travel with it through the reduction
+    double pred[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (s_src_ok) {
         for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
             const int ite = u / c.ntb, itb = u - ite * c.ntb;
@@ -269,38 +272,64 @@ mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, Loo
                                                  o.v_next, soc2, t2);
             if (!(jn < c.j_inf)) continue;
             const double f = stage_cost(o.mf, o.dt_move, c.gamma) + (1.0 - c.gamma) * wait + jn;
-            if (bestu < 0 || f < bestf) { bestf = f; bestu = u; }
+            if (bestu < 0 || f < bestf) {
+                bestf = f; bestu = u;
+                pred[0] = o.v_next; pred[1] = soc2; pred[2] = t2;    // the solver's predicted next state
+                pred[3] = o.dt_move; pred[4] = o.mf; pred[5] = o.accel;
+            }
         }
     }
-    // lexicographic (f, u) min == first win in scan order (mpc.py:269)
+    // lexicographic (f, u) min == first win in scan order (mpc.py:269); the
+    // winner's predicted state travels with it (no re-evaluation afterwards)
     for (int o = 16; o > 0; o >>= 1) {
         const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
         const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
-        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) { bestf = f2; bestu = u2; }
+        double p2[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) p2[i] = __shfl_down_sync(0xffffffffu, pred[i], o);
+        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) {
+            bestf = f2; bestu = u2;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) pred[i] = p2[i];
+        }
     }
-    if ((threadIdx.x & 31) == 0) { s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu; }
+    __shared__ double s_pred[kDecideThreads / 32][6];
+    if ((threadIdx.x & 31) == 0) {
+        s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) s_pred[threadIdx.x >> 5][i] = pred[i];
+    }
     __syncthreads();
     if (threadIdx.x != 0) return;
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
         const int u2 = s_u[w];
         const double f2 = s_f[w];
-        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) { bestf = f2; bestu = u2; }
+        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) {
+            bestf = f2; bestu = u2;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) pred[i] = s_pred[w][i];
+        }
     }
     EcoTrajRow row{};
     row.s = s; row.v = v; row.soc = soc; row.t = t; row.horizon = h;
     double te = 0.0, tb = 0.0, brake = 0.0;
-    double pred[3] = {0.0, 0.0, 0.0};
     if (bestu >= 0) {
+        // propagate_state_full (plant.py:341-439) of an admissible winner is
+        // its candidate evaluation: the same step_eval arithmetic with brake
+        // 0 (the comfort box only gates feasibility, which it passed), the
+        // same battery current, the same wait / departure clock -- so the
+        // plant step is the prediction exactly (mpc.py:575-582 holds by
+        // construction) and is not re-run here
         te = c.te_axis[bestu / c.ntb];
         tb = c.tb_axis[bestu % c.ntb];
         row.cost_to_go = bestf;
-        // re-evaluate the winner for the predicted state (same arithmetic)
-        const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, r.accel_min, r.accel_max, 0.0, q);
-        double cur;
-        battery_current(P, o.p_bat, soc, &cur);
-        pred[0] = o.v_next;
-        pred[1] = soc - o.dt_move * cur / P.c_nom;
-        pred[2] = t_base + o.dt_move;
+        row.t_eng = te; row.t_bsg = tb; row.brake_force = 0.0;
+        row.gear = q.d.gear;
+        row.wait_s = wait; row.dt_move_s = pred[3]; row.fuel_inc_g = pred[4] * pred[3]; row.accel = pred[5];
+        rows[st->n_rows] = row;
+        st->n_rows += 1;
+        st->x[0] = pred[0]; st->x[1] = pred[1]; st->x[2] = pred[2];
+        return;
     } else {
         // _max_braking_decision mpc.py:490-510
         if (v <= 0.0) { st->status = ECO_RUN_INFEASIBLE; st->status_node = s; return; }
@@ -342,9 +371,6 @@ mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, Loo
     double cur;
     if (!battery_current(P, o.p_bat, soc, &cur)) { st->status = ECO_RUN_PLANT; st->status_node = s; return; }
     const double nx0 = o.v_next, nx1 = soc - o.dt_move * cur / P.c_nom, nx2 = tb_p + o.dt_move;
-    if (bestu >= 0 && !(pred[0] == nx0 && pred[1] == nx1 && pred[2] == nx2)) {
-        st->status = 3; st->status_node = s; return;                     // mpc.py:575-582
-    }
     row.t_eng = te; row.t_bsg = tb; row.brake_force = brake;
     row.gear = q.d.gear;
     row.wait_s = wait_p; row.dt_move_s = o.dt_move; row.fuel_inc_g = o.mf * o.dt_move; row.accel = o.accel;
