@@ -404,7 +404,17 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
         ECO_CUDA(cudaLaunchKernelEx(&lc, k, a));
     } else {
         set_smem_attr(field_stage_kernel<Real>, tc.smem);
-        field_stage_kernel<Real><<<grid, block, tc.smem, st>>>(a);
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(block);
+        lc.dynamicSmemBytes = tc.smem;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = env_int("ECO_PDL", 1) ? 1 : 0;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        ECO_CUDA(cudaLaunchKernelEx(&lc, field_stage_kernel<Real>, a));
     }
     ECO_CUDA(cudaGetLastError());
 }

@@ -1227,6 +1227,7 @@ bellman_batch_kernel(BatchArgs<Real> ba) {
 template <typename Real>
 __global__ void __launch_bounds__(1024)
 field_stage_kernel(StageArgs<Real> a) {
+    pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem[];
     const int iv = blockIdx.x;
     const int nx = a.nx;
@@ -1244,17 +1245,23 @@ field_stage_kernel(StageArgs<Real> a) {
     if (jx < nx) {
         const ActRec<Real>* acts = a.act + (size_t)iv * a.U;
         const RowRec<Real>* rows = a.row + a.row_off[iv] + jx;
-        // kFU actions per round: their record loads are in flight together
+        // kFU actions per round: their record loads are in flight together;
+        // round 0's (route geometry) before waiting for the previous node
         constexpr int kFU = 4;
-        for (int k0 = slice; k0 < count; k0 += kFU * a.slices) {
-            RowRec<Real> ro[kFU];
-            ActRec<Real> rc[kFU];
+        RowRec<Real> ro[kFU];
+        ActRec<Real> rc[kFU];
+        auto fetch = [&](int k0) {
 #pragma unroll
             for (int q = 0; q < kFU; ++q) {
                 const int k = k0 + q * a.slices;
                 if (k < count) { ro[q] = rows[(size_t)k * nx]; rc[q] = acts[k]; }
                 else ro[q].off = -1;
             }
+        };
+        fetch(slice);
+        pdl_wait();
+        for (int k0 = slice; k0 < count; k0 += kFU * a.slices) {
+            if (k0 != slice) fetch(k0);
 #pragma unroll
             for (int q = 0; q < kFU; ++q) {
                 const int k = k0 + q * a.slices;
