@@ -12,6 +12,8 @@
 #include <string>
 #include <algorithm>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <vector>
 
@@ -164,6 +166,60 @@ struct EventTimer {
         return m;
     }
 };
+
+// Large device -> pageable-host copies (the J / P stacks of fine-grid solves,
+// batch tables): double-buffered pinned staging; chunk i's host-side copy is
+// spread over threads (first-touching the destination in parallel) while
+// chunk i + 1's DMA runs.  Completes before returning.
+void download_big(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    constexpr size_t kChunk = size_t(64) << 20;
+    if (bytes < (size_t(32) << 20) || std::getenv("ECO_PLAIN_D2H")) {
+        if (bytes) ECO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    static std::mutex mu;
+    static char* stage[2] = {nullptr, nullptr};
+    static cudaEvent_t ev[2];
+    std::lock_guard<std::mutex> lock(mu);
+    if (!stage[0]) {
+        for (int b = 0; b < 2; ++b) {
+            ECO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), kChunk, cudaHostAllocDefault));
+            ECO_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+        }
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nthr = (int)std::max(1u, std::min(16u, hw ? hw : 1u));
+    auto host_copy = [&](char* d, const char* s, size_t n) {
+        std::vector<std::thread> th;
+        const size_t per = (n + nthr - 1) / nthr;
+        for (int t = 0; t < nthr; ++t) {
+            const size_t a = (size_t)t * per;
+            if (a >= n) break;
+            const size_t m = std::min(per, n - a);
+            th.emplace_back([=] { std::memcpy(d + a, s + a, m); });
+        }
+        for (auto& x : th) x.join();
+    };
+    char* out = static_cast<char*>(dst);
+    const char* in = static_cast<const char*>(src);
+    int prev = -1;
+    size_t prev_off = 0, prev_n = 0, off = 0;
+    for (int i = 0; off < bytes; ++i) {
+        const size_t n = std::min(kChunk, bytes - off);
+        const int b = i & 1;
+        ECO_CUDA(cudaMemcpyAsync(stage[b], in + off, n, cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaEventRecord(ev[b], st));
+        if (prev >= 0) {
+            ECO_CUDA(cudaEventSynchronize(ev[prev]));
+            host_copy(out + prev_off, stage[prev], prev_n);
+        }
+        prev = b; prev_off = off; prev_n = n;
+        off += n;
+    }
+    ECO_CUDA(cudaEventSynchronize(ev[prev]));
+    host_copy(out + prev_off, stage[prev], prev_n);
+}
 
 inline int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -755,8 +811,8 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     ECO_CUDA(cudaGetLastError());
     ++launches;
     all.stop(st);
-    d_tmp.download(J_stack, ns * (H + 1), st);
-    d_P.download(P_stack, ns * H, st);
+    download_big(J_stack, d_tmp.p, ns * (H + 1) * sizeof(double), st);
+    download_big(P_stack, d_P.p, ns * H * sizeof(int32_t), st);
     unsigned long long live = 0;
     ECO_CUDA(cudaMemcpyAsync(&live, d_live.p, sizeof live, cudaMemcpyDeviceToHost, st));
     ECO_CUDA(cudaStreamSynchronize(st));
@@ -1395,10 +1451,8 @@ struct Batch : BatchBase {
             if (pending < 0) return;
             const int b = pending & 1;
             ECO_CUDA(cudaStreamWaitEvent(st_out, ev_out[b], 0));
-            if (J0) ECO_CUDA(cudaMemcpyAsync(J0 + (size_t)pend_c0 * ns, J0_d[b].p, (size_t)pend_B * ns * sizeof(double),
-                                             cudaMemcpyDeviceToHost, st_out));
-            if (P0) ECO_CUDA(cudaMemcpyAsync(P0 + (size_t)pend_c0 * ns, P0_d[b].p, (size_t)pend_B * ns * sizeof(int32_t),
-                                             cudaMemcpyDeviceToHost, st_out));
+            if (J0) download_big(J0 + (size_t)pend_c0 * ns, J0_d[b].p, (size_t)pend_B * ns * sizeof(double), st_out);
+            if (P0) download_big(P0 + (size_t)pend_c0 * ns, P0_d[b].p, (size_t)pend_B * ns * sizeof(int32_t), st_out);
             ECO_CUDA(cudaStreamSynchronize(st_out));
             pending = -1;
         };
@@ -1725,8 +1779,8 @@ struct Slab : SlabBase {
             ++launches;
         }
         all.stop(st);
-        if (J_stack) tmp.download(J_stack, ns * (H + 1), st);
-        if (P_slab) P.download(P_slab, (size_t)H * slab_ns, st);
+        if (J_stack) download_big(J_stack, tmp.p, ns * (H + 1) * sizeof(double), st);
+        if (P_slab) download_big(P_slab, P.p, (size_t)H * slab_ns * sizeof(int32_t), st);
         int herr = 0;
         unsigned long long nlive = 0;
         ECO_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
