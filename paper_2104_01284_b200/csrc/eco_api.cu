@@ -715,6 +715,20 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     SolveSync ssync;
     const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
                             !tcs[0].wide;
+    // large outputs (fine grids): overlap each level's D2H with the later stages
+    const bool overlap = !tabs && !persistent && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
+                         ns * (size_t)(H + 1) * sizeof(double) > (size_t(256) << 20);
+    static cudaStream_t ovs = nullptr;
+    static std::vector<cudaEvent_t> lvl_ev;
+    if (overlap) {
+        if (!ovs) ECO_CUDA(cudaStreamCreateWithFlags(&ovs, cudaStreamNonBlocking));
+        while ((int)lvl_ev.size() < H + 1) {
+            cudaEvent_t e;
+            ECO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            lvl_ev.push_back(e);
+        }
+        ECO_CUDA(cudaEventRecord(lvl_ev[H], st));       // the terminal level is in place
+    }
     sweep.start(st);
     if (persistent) {
         SolveArgs<Real> sa = solve_args(G, tcs[0], nt);
@@ -790,6 +804,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             a.dbg = dbgbuf.p;
         }
         launch_stage<Real, 0>(a, tc, count, st);
+        if (overlap) ECO_CUDA(cudaEventRecord(lvl_ev[k], st));
         if (dbg_on) {
             std::vector<unsigned long long> h(dbgbuf.n);
             dbgbuf.download(h.data(), h.size(), st);
@@ -807,12 +822,29 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         ++launches;
     }
     sweep.stop(st);
-    to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, H + 1, pr->j_inf);
-    ECO_CUDA(cudaGetLastError());
-    ++launches;
-    all.stop(st);
-    download_big(J_stack, d_tmp.p, ns * (H + 1) * sizeof(double), st);
-    download_big(P_stack, d_P.p, ns * H * sizeof(int32_t), st);
+    if (overlap) {
+        // level k is final once stage k ran: its conversion and download run
+        // on a side stream while the remaining stages sweep
+        all.stop(st);
+        for (int k = H; k >= 0; --k) {
+            ECO_CUDA(cudaStreamWaitEvent(ovs, lvl_ev[k], 0));
+            to_external_levels_kernel<Real><<<grid_for(ns), 256, 0, ovs>>>(d_J.p + (size_t)k * LV,
+                                                                           d_tmp.p + (size_t)k * ns, ns, 1,
+                                                                           pr->j_inf);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
+            download_big(J_stack + (size_t)k * ns, d_tmp.p + (size_t)k * ns, ns * sizeof(double), ovs);
+            if (k < H) download_big(P_stack + (size_t)k * ns, d_P.p + (size_t)k * ns, ns * sizeof(int32_t), ovs);
+        }
+    } else {
+        to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, H + 1,
+                                                                               pr->j_inf);
+        ECO_CUDA(cudaGetLastError());
+        ++launches;
+        all.stop(st);
+        download_big(J_stack, d_tmp.p, ns * (H + 1) * sizeof(double), st);
+        download_big(P_stack, d_P.p, ns * H * sizeof(int32_t), st);
+    }
     unsigned long long live = 0;
     ECO_CUDA(cudaMemcpyAsync(&live, d_live.p, sizeof live, cudaMemcpyDeviceToHost, st));
     ECO_CUDA(cudaStreamSynchronize(st));
