@@ -21,6 +21,7 @@ from .plant import ActionVector, StateVector, Vehicle
 from .route import Route, SignalTiming, SpatSchedule, load_route, next_green_start, phase_at
 from .batch import BatchResult, BatchSolver, solve_batch
 from .slab import SlabResult, SlabSolver, gather_policies, make_partition
+from .harness import BenchReport, DiffReport, compare_solves, diff_backends_run, run_bench
 from .io import read_trajectory_csv, summarize, write_summary_json, write_timing_csv, write_trajectory_csv
 
 __version__ = "0.1.0"

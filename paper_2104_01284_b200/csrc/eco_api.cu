@@ -583,54 +583,99 @@ struct TablesDev {
 };
 
 // --------------------------------------------------------- horizon solve
-// Per-solve inputs of a horizon solve on the device: plant, the H step
-// plans (DevPlan + source speed axis + ladders) and the axes.
+// Per-solve inputs of a horizon solve: plant, the H step plans (DevPlan +
+// source speed axis + ladders + stage flags + source kinds), the axes and the
+// terminal level, packed into one pinned host block and sent with a single
+// copy into a grow-only device block, so repeated solves allocate nothing.
 struct HorizonInputs {
-    DBuf<EcoPlant> plant;
-    DBuf<DevPlan> plans;
-    DBuf<double> v, tdep, wait, te, tb, soc;
-    DBuf<uint8_t> green, dep;
-    DBuf<int> flags;           // kStageAny* per stage
-    void upload(const EcoPlant* p, const EcoProblem* pr, const EcoStepPlan* pl, int H, cudaStream_t st) {
-        const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t;
-        std::vector<DevPlan> hp(H);
-        std::vector<double> hv((size_t)H * nv);
-        std::vector<uint8_t> hgreen((size_t)H * nt), hdep((size_t)H * nt);
-        std::vector<double> htdep((size_t)H * nt), hwait((size_t)H * nt);
-        std::vector<int> hflags(H, 0);
+    DBuf<char> blob;
+    char* host = nullptr;
+    size_t host_cap = 0;
+    EcoPlant* plant = nullptr;
+    DevPlan* plans = nullptr;
+    double *v = nullptr, *tdep = nullptr, *wait = nullptr, *te = nullptr, *tb = nullptr, *soc = nullptr;
+    double* terminal = nullptr;
+    uint8_t *green = nullptr, *dep = nullptr;
+    int* flags = nullptr;      // kStageAny* per stage
+    int8_t* kinds = nullptr;   // source node kind per stage
+    HorizonInputs() = default;
+    HorizonInputs(const HorizonInputs&) = delete;
+    HorizonInputs& operator=(const HorizonInputs&) = delete;
+    ~HorizonInputs() {
+        if (host) cudaFreeHost(host);
+    }
+    // every caller synchronises its stream before returning, so the host
+    // block is free again when the next upload fills it
+    void upload(const EcoPlant* p, const EcoProblem* pr, const EcoStepPlan* pl, int H, const double* term,
+                cudaStream_t st) {
+        const size_t nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t, ns = nv * nx * nt;
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            const size_t o = off;
+            off += (bytes + 255) & ~size_t(255);
+            return o;
+        };
+        const size_t o_plant = take(sizeof(EcoPlant)), o_plans = take(sizeof(DevPlan) * H),
+                     o_v = take(sizeof(double) * H * nv), o_tdep = take(sizeof(double) * H * nt),
+                     o_wait = take(sizeof(double) * H * nt), o_te = take(sizeof(double) * pr->n_te),
+                     o_tb = take(sizeof(double) * pr->n_tb), o_soc = take(sizeof(double) * nx),
+                     o_term = take(term ? sizeof(double) * ns : 0), o_green = take((size_t)H * nt),
+                     o_dep = take((size_t)H * nt), o_flags = take(sizeof(int) * H), o_kinds = take(H);
+        if (off > host_cap) {
+            if (host) cudaFreeHost(host);
+            host = nullptr;
+            host_cap = 0;
+            ECO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host), off, cudaHostAllocDefault));
+            host_cap = off;
+        }
+        blob.ensure(off);
+        char* h = host;
+        std::memcpy(h + o_plant, p, sizeof(EcoPlant));
+        DevPlan* hp = reinterpret_cast<DevPlan*>(h + o_plans);
+        int* hflags = reinterpret_cast<int*>(h + o_flags);
         for (int k = 0; k < H; ++k) {
             const EcoStepPlan& s = pl[k];
             if (!s.v_src || !s.arr_green || !s.dep_ok || !s.t_dep || !s.wait) throw ArgError{"null plan array"};
             hp[k] = dev_plan(s);
-            for (int z = 0; z < nt; ++z) {
-                if (s.arr_green[z] == 0) hflags[k] |= kStageAnyRed;
-                if (s.dep_ok[z] == 0 || s.wait[z] > 0.0) hflags[k] |= kStageAnyHold;
+            int f = 0;
+            for (size_t z = 0; z < nt; ++z) {
+                if (s.arr_green[z] == 0) f |= kStageAnyRed;
+                if (s.dep_ok[z] == 0 || s.wait[z] > 0.0) f |= kStageAnyHold;
             }
-            std::memcpy(&hv[(size_t)k * nv], s.v_src, sizeof(double) * nv);
-            std::memcpy(&hgreen[(size_t)k * nt], s.arr_green, nt);
-            std::memcpy(&hdep[(size_t)k * nt], s.dep_ok, nt);
-            std::memcpy(&htdep[(size_t)k * nt], s.t_dep, sizeof(double) * nt);
-            std::memcpy(&hwait[(size_t)k * nt], s.wait, sizeof(double) * nt);
+            hflags[k] = f;
+            reinterpret_cast<int8_t*>(h + o_kinds)[k] = (int8_t)s.src_kind;
+            std::memcpy(h + o_v + sizeof(double) * k * nv, s.v_src, sizeof(double) * nv);
+            std::memcpy(h + o_green + (size_t)k * nt, s.arr_green, nt);
+            std::memcpy(h + o_dep + (size_t)k * nt, s.dep_ok, nt);
+            std::memcpy(h + o_tdep + sizeof(double) * k * nt, s.t_dep, sizeof(double) * nt);
+            std::memcpy(h + o_wait + sizeof(double) * k * nt, s.wait, sizeof(double) * nt);
         }
-        plant.ensure(1);
-        plant.upload(p, 1, st);
-        plans.ensure(H); v.ensure((size_t)H * nv); tdep.ensure((size_t)H * nt); wait.ensure((size_t)H * nt);
-        green.ensure((size_t)H * nt); dep.ensure((size_t)H * nt); flags.ensure(H);
-        flags.upload(hflags.data(), H, st);
-        te.ensure(pr->n_te); tb.ensure(pr->n_tb); soc.ensure(nx);
-        plans.upload(hp.data(), H, st);
-        v.upload(hv.data(), hv.size(), st);
-        green.upload(hgreen.data(), hgreen.size(), st);
-        dep.upload(hdep.data(), hdep.size(), st);
-        tdep.upload(htdep.data(), htdep.size(), st);
-        wait.upload(hwait.data(), hwait.size(), st);
-        te.upload(pr->te_axis, pr->n_te, st);
-        tb.upload(pr->tb_axis, pr->n_tb, st);
-        soc.upload(pr->soc_axis, nx, st);
-        // pageable sources: the copies must finish before the vectors go
-        ECO_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(h + o_te, pr->te_axis, sizeof(double) * pr->n_te);
+        std::memcpy(h + o_tb, pr->tb_axis, sizeof(double) * pr->n_tb);
+        std::memcpy(h + o_soc, pr->soc_axis, sizeof(double) * nx);
+        if (term) std::memcpy(h + o_term, term, sizeof(double) * ns);
+        ECO_CUDA(cudaMemcpyAsync(blob.p, host, off, cudaMemcpyHostToDevice, st));
+        char* d = blob.p;
+        plant = reinterpret_cast<EcoPlant*>(d + o_plant);
+        plans = reinterpret_cast<DevPlan*>(d + o_plans);
+        v = reinterpret_cast<double*>(d + o_v);
+        tdep = reinterpret_cast<double*>(d + o_tdep);
+        wait = reinterpret_cast<double*>(d + o_wait);
+        te = reinterpret_cast<double*>(d + o_te);
+        tb = reinterpret_cast<double*>(d + o_tb);
+        soc = reinterpret_cast<double*>(d + o_soc);
+        terminal = term ? reinterpret_cast<double*>(d + o_term) : nullptr;
+        green = reinterpret_cast<uint8_t*>(d + o_green);
+        dep = reinterpret_cast<uint8_t*>(d + o_dep);
+        flags = reinterpret_cast<int*>(d + o_flags);
+        kinds = reinterpret_cast<int8_t*>(d + o_kinds);
     }
 };
+
+inline HorizonInputs& horizon_inputs() {
+    static HorizonInputs in;
+    return in;
+}
 
 template <typename Real>
 struct HorizonWorkspace {
@@ -661,12 +706,8 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     const size_t ns = (size_t)nv * nx * nt;
     cudaStream_t st = 0;
     int64_t launches = 0;
-    HorizonInputs in;
-    in.upload(plant, pr, plans, H, st);
-    DBuf<EcoPlant>& d_plant = in.plant;
-    DBuf<DevPlan>& d_plans = in.plans;
-    DBuf<double>&d_v = in.v, &d_tdep = in.tdep, &d_wait = in.wait, &d_te = in.te, &d_tb = in.tb, &d_soc = in.soc;
-    DBuf<uint8_t>&d_green = in.green, &d_dep = in.dep;
+    HorizonInputs& in = horizon_inputs();
+    in.upload(plant, pr, plans, H, terminal, st);
     TablesDev tdev;   // plant path: no tables
 
     // device buffers persist across calls (grow-only workspace): repeated
@@ -684,13 +725,12 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     DBuf<double>& d_tmp = W.tmp;
     DBuf<unsigned long long>& d_live = W.live;
     ECO_CUDA(cudaMemsetAsync(d_live.p, 0, sizeof(unsigned long long), st));
-    d_tmp.upload(terminal, ns, st);
 
     EventTimer all, sweep;
     all.start(st);
     // toy mode: each step has its own table; geometry built per plan below
-    if (!tabs) build_geometry(G, d_plant.p, d_plans.p, d_v.p, d_te.p, d_tb.p, d_soc.p, tdev.view, st, &launches);
-    to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(d_tmp.p, d_J.p + (size_t)H * LV, ns, pr->j_inf);
+    if (!tabs) build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+    to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(in.terminal, d_J.p + (size_t)H * LV, ns, pr->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++launches;
     double sweep_ms = 0.0;
@@ -701,21 +741,19 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             tk.upload(&tabs[k], (size_t)nv * U, st);
             toyG[k].dims = GeomDims{1, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max,
                                     pr->gamma, pr->dtg};
-            build_geometry(toyG[k], d_plant.p, d_plans.p + k, d_v.p + (size_t)k * nv, d_te.p, d_tb.p, d_soc.p,
+            build_geometry(toyG[k], in.plant, in.plans + k, in.v + (size_t)k * nv, in.te, in.tb, in.soc,
                            tk.view, st, &launches);
             ECO_CUDA(cudaStreamSynchronize(st));   // tk freed at scope end
         }
     }
     std::vector<TileCfg> tcs(H);
     for (int k = 0; k < H; ++k) tcs[k] = tile_cfg(tabs ? toyG[k] : G, nt, 0);
-    std::vector<int8_t> hkinds(H);
-    for (int k = 0; k < H; ++k) hkinds[k] = (int8_t)plans[k].src_kind;
-    DBuf<int8_t> d_kinds(H);
-    d_kinds.upload(hkinds.data(), H, st);
     SolveSync ssync;
     const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
                             !tcs[0].wide;
-    // large outputs (fine grids): overlap each level's D2H with the later stages
+    // large outputs (fine grids): overlap each level's D2H with the later
+    // stages.  Small stacks go in one copy at the end: per-level pageable
+    // copies cost more than they hide (C2: 1.67 vs 1.16 ms per solve call)
     const bool overlap = !tabs && !persistent && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
                          ns * (size_t)(H + 1) * sizeof(double) > (size_t(256) << 20);
     static cudaStream_t ovs = nullptr;
@@ -736,12 +774,12 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         sa.base.t0 = pr->t0;
         sa.base.dtg = pr->dtg;
         sa.base.j_inf = (Real)pr->j_inf;
-        sa.vaxes = d_v.p;
-        sa.src_kinds = d_kinds.p;
+        sa.vaxes = in.v;
+        sa.src_kinds = in.kinds;
         sa.plan0 = 0;
         sa.H = H;
         sa.green_shift = 0;
-        sa.green = d_green.p; sa.dep_ok = d_dep.p; sa.t_dep = d_tdep.p; sa.wait = d_wait.p;
+        sa.green = in.green; sa.dep_ok = in.dep; sa.t_dep = in.tdep; sa.wait = in.wait;
         sa.J = d_J.p; sa.LV = LV; sa.LC = LC;
         sa.P = d_P.p; sa.PV = ns;
         DBuf<unsigned long long> dbgbuf;
@@ -779,13 +817,13 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     }
     for (int k = H - 1; k >= 0 && !persistent; --k) {
         const TileCfg& tc = tcs[k];
-        StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, d_v.p + (size_t)k * nv, nt, tc)
-                                 : stage_args(G, k, d_v.p + (size_t)k * nv, nt, tc);
-        a.green = d_green.p + (size_t)k * nt;
-        a.dep_ok = d_dep.p + (size_t)k * nt;
-        a.t_dep = d_tdep.p + (size_t)k * nt;
-        a.wait = d_wait.p + (size_t)k * nt;
-        a.flags = in.flags.p + k;
+        StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, in.v + (size_t)k * nv, nt, tc)
+                                 : stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
+        a.green = in.green + (size_t)k * nt;
+        a.dep_ok = in.dep + (size_t)k * nt;
+        a.t_dep = in.tdep + (size_t)k * nt;
+        a.wait = in.wait + (size_t)k * nt;
+        a.flags = in.flags + k;
         a.J_next = d_J.p + (size_t)(k + 1) * LV;
         a.J_next1 = a.J_next + LC;
         a.J_out = d_J.p + (size_t)k * LV;
@@ -1624,6 +1662,7 @@ struct Slab : SlabBase {
     DBuf<unsigned> flag;               // barrier counter, IPC-exported
     DBuf<int> err;
     DBuf<int32_t> P;
+    HorizonInputs in;
     DBuf<double> tmp;
     DBuf<unsigned long long> live;
     Geometry<Real> G;
@@ -1745,11 +1784,9 @@ struct Slab : SlabBase {
         const int plo = lo[rank], phi = hi[rank];
         const size_t plane = (size_t)nx * nt, slab_ns = (size_t)(phi - plo) * plane;
         int64_t launches = 0;
-        HorizonInputs in;
-        in.upload(plant, pr, plans, H, st);
+        in.upload(plant, pr, plans, H, terminal, st);
         P.ensure((size_t)H * slab_ns);
-        tmp.ensure(ns * (size_t)(J_stack ? H + 1 : 1));
-        tmp.upload(terminal, ns, st);
+        if (J_stack) tmp.ensure(ns * (size_t)(H + 1));
         ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
         EventTimer all, sweep;
         all.start(st);
@@ -1757,8 +1794,8 @@ struct Slab : SlabBase {
         G.plo = plo;
         G.phi = phi;
         TablesDev tdev;
-        build_geometry(G, in.plant.p, in.plans.p, in.v.p, in.te.p, in.tb.p, in.soc.p, tdev.view, st, &launches);
-        to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(tmp.p, J.p + (size_t)H * LV, ns, pr->j_inf);
+        build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+        to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(in.terminal, J.p + (size_t)H * LV, ns, pr->j_inf);
         ECO_CUDA(cudaGetLastError());
         ++launches;
         const TileCfg tc = tile_cfg(G, nt, 0);
@@ -1773,12 +1810,12 @@ struct Slab : SlabBase {
         }
         sweep.start(st);
         for (int k = H - 1; k >= 0; --k) {
-            StageArgs<Real> a = stage_args(G, k, in.v.p + (size_t)k * nv, nt, tc);
-            a.green = in.green.p + (size_t)k * nt;
-            a.flags = in.flags.p + k;
-            a.dep_ok = in.dep.p + (size_t)k * nt;
-            a.t_dep = in.tdep.p + (size_t)k * nt;
-            a.wait = in.wait.p + (size_t)k * nt;
+            StageArgs<Real> a = stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
+            a.green = in.green + (size_t)k * nt;
+            a.flags = in.flags + k;
+            a.dep_ok = in.dep + (size_t)k * nt;
+            a.t_dep = in.tdep + (size_t)k * nt;
+            a.wait = in.wait + (size_t)k * nt;
             a.J_next = J.p + (size_t)(k + 1) * LV;
             a.J_next1 = a.J_next + LC;
             a.J_out = J.p + (size_t)k * LV;
