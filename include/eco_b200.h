@@ -237,8 +237,9 @@ int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route,
  *           precomputed field instead of building it; field_out optional;
  * run     — closed loop from start_node for max_steps nodes (< 0: to the end)
  *           (simulate_closed_loop, mpc.py:513-596); flags: ECO_RUN_COUNT_LIVE
- *           counts gathers (slower), ECO_RUN_TIME_SWEEPS times the Bellman
- *           sweeps with CUDA events (stats->dominant_ms). */
+ *           counts gathers (slower).  stats->dominant_ms is always the summed
+ *           per-step solve clock (device timestamps, prepare entry -> decision
+ *           entry); ECO_RUN_TIME_SWEEPS is accepted for compatibility. */
 typedef struct EcoSession EcoSession;
 #define ECO_RUN_COUNT_LIVE 1
 #define ECO_RUN_TIME_SWEEPS 2

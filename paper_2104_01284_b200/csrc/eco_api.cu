@@ -226,6 +226,25 @@ inline int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+// Kernel launch with programmatic dependent launch (when pdl and ECO_PDL):
+// the kernel may start once the previous kernel in the stream triggered
+// griddepcontrol.launch_dependents; it must griddepcontrol.wait before
+// reading that kernel's results.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t st, bool pdl, Args&&... args) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && env_int("ECO_PDL", 1)) ? 1 : 0;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    ECO_CUDA(cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...));
+}
+
 // long time ladders take the wide-row stage path (ECO_WIDE=0 disables it)
 inline bool wide_rows(int nt) { return nt >= 128 && nt % 2 == 0 && env_int("ECO_WIDE", 1) != 0; }
 
@@ -1136,7 +1155,6 @@ struct SessionBase {
 };
 
 constexpr int kRunCountLive = 1;
-constexpr int kRunTimeSweeps = 2;
 
 template <typename Real>
 struct Session : SessionBase {
@@ -1150,6 +1168,10 @@ struct Session : SessionBase {
     DBuf<Real> field_int;          // internal (n, nv, nx)
     bool fitted = false;
     DBuf<LoopState> state;
+    DBuf<DecideCand> dec_cand;      // split decide: per-action candidate records
+    DBuf<DecideHead> dec_head;
+    cudaStream_t dec_side = nullptr;
+    cudaEvent_t dec_fork = nullptr, dec_join = nullptr;
     DBuf<uint8_t> green, dep;
     DBuf<double> tdep, wait, tax;
     DBuf<int> sflags;              // kStageAny* per stage of the current solve
@@ -1157,7 +1179,6 @@ struct Session : SessionBase {
     DBuf<int32_t> P;
     DBuf<EcoTrajRow> rows;
     DBuf<unsigned long long> live;
-    std::vector<cudaEvent_t> ev;
     SolveSync ssync;
     cudaStream_t st = 0;
     // CUDA graph of a whole closed loop (prepare / H stage sweeps / decide per
@@ -1188,16 +1209,16 @@ struct Session : SessionBase {
         P.alloc(ns);
         rows.alloc(n - 1);
         live.alloc(1);
-        ev.resize(2 * (size_t)n);
-        for (auto& e : ev) ECO_CUDA(cudaEventCreate(&e));
         ECO_CUDA(cudaStreamSynchronize(st));
         // a blocking stream of its own (stream capture is impossible on the
         // legacy default stream; blocking keeps it ordered with stream 0)
         ECO_CUDA(cudaStreamCreate(&st));
     }
     ~Session() override {
-        for (auto& e : ev) cudaEventDestroy(e);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (dec_fork) cudaEventDestroy(dec_fork);
+        if (dec_join) cudaEventDestroy(dec_join);
+        if (dec_side) cudaStreamDestroy(dec_side);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -1252,7 +1273,6 @@ struct Session : SessionBase {
         const int U = cfg.n_te * cfg.n_tb;
         const size_t ns = (size_t)nv * nx * nt;
         const bool count = flags & kRunCountLive;
-        const bool timed = flags & kRunTimeSweeps;
         int64_t launches = 0;
         LoopState h0{};
         h0.x[0] = x0[0]; h0.x[1] = x0[1]; h0.x[2] = x0[2];
@@ -1263,24 +1283,34 @@ struct Session : SessionBase {
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
         const TileCfg tc = tile_cfg(ctx.G, nt, 0);
         const bool persistent = env_int("ECO_PERSISTENT", 0) != 0 && !tc.wide;
+        if (!dec_side) {
+            ECO_CUDA(cudaStreamCreateWithFlags(&dec_side, cudaStreamNonBlocking));
+            ECO_CUDA(cudaEventCreateWithFlags(&dec_fork, cudaEventDisableTiming));
+            ECO_CUDA(cudaEventCreateWithFlags(&dec_join, cudaEventDisableTiming));
+        }
+        dec_cand.ensure((size_t)U);
+        dec_head.ensure(1);
         int64_t stages = 0;
-        int nev = 0;
-        auto enqueue = [&](cudaStream_t qs, bool capturing) {
-            // inside a graph, events are recorded as external event nodes so
-            // cudaEventElapsedTime works on them after each replay
-            const unsigned evflag = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+        auto enqueue = [&](cudaStream_t qs) {
             stages = 0;
-            nev = 0;
             launches = 0;
             for (int s = start_node; s < s_end; ++s) {
                 const int h = H < n - 1 - s ? H : n - 1 - s;
                 const size_t LV = level_stride(ns), LC = level_copy(ns);
-                mpc_prepare_kernel<Real><<<std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256)), 256, 0, qs>>>(
-                    ctx.R.view, lc, state.p, s, h, cfg.use_terminal_field ? field.p : nullptr, lad,
-                    J.p + (size_t)h * LV, J.p + (size_t)h * LV + LC);
+                launch_pdl(mpc_prepare_kernel<Real>, std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256)), 256,
+                           qs, s > start_node, ctx.R.view, lc, state.p, s, h,
+                           cfg.use_terminal_field ? (const double*)field.p : nullptr, lad, J.p + (size_t)h * LV,
+                           J.p + (size_t)h * LV + LC);
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
-                if (timed) ECO_CUDA(cudaEventRecordWithFlags(ev[2 * nev], qs, evflag));
+                // the J-independent half of the decision runs beside the sweeps
+                ECO_CUDA(cudaEventRecord(dec_fork, qs));
+                ECO_CUDA(cudaStreamWaitEvent(dec_side, dec_fork, 0));
+                mpc_candidates_kernel<<<(U + kCandThreads - 1) / kCandThreads, kCandThreads, 0, dec_side>>>(
+                    ctx.plant.p, ctx.R.view, lc, state.p, s, lad, dec_cand.p, dec_head.p);
+                ECO_CUDA(cudaGetLastError());
+                ++launches;
+                ECO_CUDA(cudaEventRecord(dec_join, dec_side));
                 if (persistent) {
                     SolveArgs<Real> sa = solve_args(ctx.G, tc, nt);
                     sa.base.status = &state.p->status;
@@ -1322,33 +1352,33 @@ struct Session : SessionBase {
                     ++launches;
                     ++stages;
                 }
-                if (timed) ECO_CUDA(cudaEventRecordWithFlags(ev[2 * nev + 1], qs, evflag));
-                ++nev;
-                mpc_decide_kernel<Real><<<1, kDecideThreads, 0, qs>>>(ctx.plant.p, ctx.R.view, lc, state.p, s, h,
-                                                                      lad, J.p + LV, rows.p);
+                ECO_CUDA(cudaStreamWaitEvent(qs, dec_join, 0));
+                launch_pdl(mpc_pick_kernel<Real>, 1, std::min(kDecideThreads, (U + 31) / 32 * 32), qs, true,
+                           (const EcoPlant*)ctx.plant.p, ctx.R.view, lc, state.p, s, h, (const Real*)(J.p + LV),
+                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p);
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
             }
         };
         const bool use_graph = !count && !persistent && env_int("ECO_GRAPH", 1) != 0;
         if (use_graph) {
-            const std::vector<long long> key = {start_node, s_end, timed ? 1 : 0, (long long)(size_t)ctx.G.row2.p,
+            const std::vector<long long> key = {start_node, s_end, (long long)(size_t)ctx.G.row2.p,
                                                 (long long)(size_t)ctx.G.tiles.p, (long long)(size_t)ctx.G.order.p,
                                                 (long long)(size_t)field.p, tc.tj, tc.slices};
             if (!gexec || key != gkey) {
                 if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
                 cudaGraph_t graph;
                 ECO_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                enqueue(st, true);
+                enqueue(st);
                 ECO_CUDA(cudaStreamEndCapture(st, &graph));
                 ECO_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
                 cudaGraphDestroy(graph);
                 gkey = key;
             }
             // counters of the captured loop (same structure every replay)
-            stages = 0; nev = 0;
-            for (int s = start_node; s < s_end; ++s) { stages += H < n - 1 - s ? H : n - 1 - s; ++nev; }
-            launches = (int64_t)nev * 2 + stages;
+            stages = 0;
+            for (int s = start_node; s < s_end; ++s) stages += H < n - 1 - s ? H : n - 1 - s;
+            launches = (int64_t)(s_end - start_node) * 3 + stages;   // prepare, candidates, pick + stages
             all.start(st);
             state.upload(&h0, 1, st);
             ECO_CUDA(cudaGraphLaunch(gexec, st));
@@ -1356,7 +1386,7 @@ struct Session : SessionBase {
             all.start(st);
             state.upload(&h0, 1, st);
             if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
-            enqueue(st, false);
+            enqueue(st);
         }
         all.stop(st);
         LoopState hs{};
@@ -1371,14 +1401,8 @@ struct Session : SessionBase {
         *status_node = hs.status_node;
         final_state[0] = hs.x[0]; final_state[1] = hs.x[1]; final_state[2] = hs.x[2];
         if (stats) {
-            double sweep_ms = 0.0;
-            for (int i = 0; timed && i < nev; ++i) {
-                float m = 0.f;
-                ECO_CUDA(cudaEventElapsedTime(&m, ev[2 * i], ev[2 * i + 1]));
-                sweep_ms += m;
-            }
             stats->device_ms = all.ms();
-            stats->dominant_ms = timed ? sweep_ms : -1.0;
+            stats->dominant_ms = (double)hs.sweep_ns * 1e-6;   // summed per-step solve clocks
             stats->dense_updates = stages * (int64_t)ns * U;
             stats->live_updates = count ? (int64_t)nlive : -1;
             stats->stages = stages;
@@ -2009,7 +2033,7 @@ int32_t eco_mpc_run(const EcoPlant* plant, const EcoRoute* route, const EcoMpcCo
         std::unique_ptr<SessionBase> s(make_session(plant, route, cfg));
         s->fit(field_in, field_out, nullptr);
         s->run(cfg->start_node, cfg->max_steps, x_start, rows, n_rows, status, status_node, final_state,
-               kRunTimeSweeps, stats);
+               0, stats);
     });
 }
 

@@ -14,6 +14,12 @@
 
 namespace eco {
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct DevRoute {               // device copies of EcoRoute arrays
     int n;
     double delta_d, accel_min, accel_max, stop_dwell;
@@ -35,6 +41,8 @@ struct LoopState {              // lives in device memory for the whole run
     int32_t status_node;
     int32_t n_rows;
     int32_t pad;
+    unsigned long long prep_ns;     // globaltimer at this step's prepare entry
+    unsigned long long sweep_ns;    // summed prepare-entry -> pick-entry clocks
 };
 
 struct Ladders {                // [H+1][nt] per receding-horizon solve
@@ -121,9 +129,13 @@ __device__ __forceinline__ Real terminal_value(double base, double soc, double t
 // and the terminal level J_h (all blocks; grid-stride over (v, soc) cells,
 // each replicated along t, both level copies).
 template <typename Real>
-__global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, const LoopState* st, int s, int h,
+__global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, LoopState* st, int s, int h,
                                    const double* field, Ladders lad, Real* Jh, Real* Jh1) {
+    pdl_wait();           // launched programmatically after the previous step's pick
     if (st->status != 0) return;
+    // per-step solve clock, prepare entry -> pick entry: device timestamps
+    // instead of event nodes, which cost ~20 us per step inside the graph
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->prep_ns = globaltimer_ns();
     const double t = st->x[2];
     const double t0 = c.dt * floor(t / c.dt);          // GridSpec.t_axis dp.py:75-77
     const int nt = c.nt;
@@ -197,156 +209,179 @@ __device__ double table_interp(const Real* J, const double* va, int nv, const do
 
 constexpr int kDecideThreads = 1024;
 
-// One block of kDecideThreads.  argmin over the action grid at the exact
-// state on level J_1 (the solve's tables[1]), then the plant step.
-template <typename Real>
-__global__ void __launch_bounds__(kDecideThreads)
-mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
-                  Ladders lad, const Real* J1, EcoTrajRow* rows) {
-    if (st->status != 0) return;
-    // the plant (20 KB of maps and axes) is read by every candidate's step
-    // evaluation: one cooperative copy into shared memory
-    __shared__ __align__(16) EcoPlant s_plant;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(plant);
-        uint4* dst = reinterpret_cast<uint4*>(&s_plant);
-        for (int i = threadIdx.x; i < (int)(sizeof(EcoPlant) / 16); i += blockDim.x) dst[i] = src[i];
-        if (threadIdx.x == 0)
-            for (int i = (int)(sizeof(EcoPlant) / 16) * 16; i < (int)sizeof(EcoPlant); ++i)
-                reinterpret_cast<char*>(&s_plant)[i] = reinterpret_cast<const char*>(plant)[i];
+
+// The MPC decision (mpc.py:189-278 + 490-510, plant.py:341-439), in two
+// kernels.  Everything of the exact-state argmin that does not read the
+// solve's tables -- the source-node wait, the plant step of every candidate
+// action, its battery current and the floor-sample green gate -- runs in
+// mpc_candidates_kernel on a side branch of the MPC step, concurrently with
+// the H stage sweeps; mpc_pick_kernel then interpolates J_1 (the solve's
+// tables[1]) at each admissible candidate's successor, reduces (f, u)
+// lexicographically (= the first win in scan order, mpc.py:269) and applies
+// the winner.  For an admissible winner propagate_state_full is its
+// candidate evaluation: the same step_eval arithmetic with brake 0 (the
+// comfort box only gates feasibility, which it passed), the same battery
+// current and departure clock -- so the plant step is the prediction exactly
+// (mpc.py:575-582 holds by construction) and is not re-run.
+struct DecideCand {            // one candidate action (64 B)
+    double pre;                // stage cost + (1 - gamma) * wait
+    double v2, soc2, t2, dt_move, mf, accel;
+    double ok;                 // 1: admissible before the table lookup
+};
+struct DecideHead {            // per-step header (block 0, thread 0)
+    double wait, t_base;
+    int src_ok, gear;
+};
+
+__device__ __forceinline__ int decide_source(const DevRoute& r, const LoopCfg& c, int s, int src, double v, double t,
+                                             double* wait_out, double* t_base_out) {
+    double wait = 0.0, t_base = t;
+    int ok = 1;
+    if (src == ECO_NODE_STOP) {
+        if (v > 0.0) ok = 0;
+        wait = r.stop_dwell;
+        t_base = t + wait;
+    } else if (src == ECO_NODE_SIGNAL && v == 0.0) {
+        const double* win = r.sig_win + (size_t)s * ECO_MAX_WINDOWS * 2;
+        if (!sig_is_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t)) {
+            if (!c.teleport) ok = 0;
+            t_base = sig_next_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t);
+            wait = t_base - t;
+        }
     }
-    __syncthreads();
-    const EcoPlant& P = s_plant;
-    __shared__ double s_f[kDecideThreads / 32];
-    __shared__ int s_u[kDecideThreads / 32];
-    __shared__ double s_wait, s_tbase;
-    __shared__ int s_src_ok;
+    *wait_out = wait;
+    *t_base_out = t_base;
+    return ok;
+}
+
+constexpr int kCandThreads = 128;
+
+__global__ void __launch_bounds__(kCandThreads)
+mpc_candidates_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, const LoopState* st, int s,
+                      Ladders lad, DecideCand* cand, DecideHead* head) {
+    if (st->status != 0) return;
+    const EcoPlant& P = *plant;
     const double v = st->x[0], soc = st->x[1], t = st->x[2];
     const int src = r.kinds[s], dst = r.kinds[s + 1];
-    if (threadIdx.x == 0) {
-        double wait = 0.0, t_base = t;
-        int ok = 1;
-        if (src == ECO_NODE_STOP) {
-            if (v > 0.0) ok = 0;
-            wait = r.stop_dwell;
-            t_base = t + wait;
-        } else if (src == ECO_NODE_SIGNAL && v == 0.0) {
-            const double* win = r.sig_win + (size_t)s * ECO_MAX_WINDOWS * 2;
-            if (!sig_is_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t)) {
-                if (!c.teleport) ok = 0;
-                t_base = sig_next_green(r.sig_cycle[s], r.sig_offset[s], win, r.sig_nwin[s], t);
-                wait = t_base - t;
+    double wait, t_base;
+    const int src_ok = decide_source(r, c, s, src, v, t, &wait, &t_base);
+    const StepPre q = step_pre(P, v, r.cos_g[s], r.sin_g[s]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        head->wait = wait; head->t_base = t_base; head->src_ok = src_ok; head->gear = q.d.gear;
+    }
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= c.U) return;
+    DecideCand k{};
+    k.ok = 0.0;
+    if (src_ok) {
+        const int ite = u / c.ntb, itb = u - ite * c.ntb;
+        const double te = c.te_axis[ite], tb = c.tb_axis[itb];
+        if (!(te > q.te_hi || te < q.te_lo || tb > q.tb_hi || tb < q.tb_lo)) {
+            const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, r.accel_min, r.accel_max, 0.0, q);
+            double cur;
+            if (o.feas == kFeasOk && !(o.clamped && dst == ECO_NODE_PLAIN) && !(dst == ECO_NODE_STOP && o.v_next > 0.0) &&
+                battery_current(P, o.p_bat, soc, &cur)) {
+                const double soc2 = soc - o.dt_move * cur / P.c_nom;
+                const double t2 = t_base + o.dt_move;
+                bool gate = true;
+                if (o.v_next > 0.0) {            // floor-sample green gate mpc.py:256-261
+                    int zlo, zhi;
+                    double w;
+                    if (locate_uniform(t2, lad.t_axis[0], c.dt, c.nt, &zlo, &zhi, &w) && lad.green[c.nt + zlo] == 0)
+                        gate = false;
+                }
+                if (gate) {
+                    k.pre = stage_cost(o.mf, o.dt_move, c.gamma) + (1.0 - c.gamma) * wait;
+                    k.v2 = o.v_next; k.soc2 = soc2; k.t2 = t2;
+                    k.dt_move = o.dt_move; k.mf = o.mf; k.accel = o.accel;
+                    k.ok = 1.0;
+                }
             }
         }
-        s_wait = wait; s_tbase = t_base; s_src_ok = ok;
     }
-    __syncthreads();
-    const double wait = s_wait, t_base = s_tbase;
-    const StepPre q = step_pre(P, v, r.cos_g[s], r.sin_g[s]);
+    cand[u] = k;
+}
+
+__device__ __forceinline__ bool decide_better(double f2, int u2, double f, int u) {
+    return u2 >= 0 && (u < 0 || f2 < f || (f2 == f && u2 < u));
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kDecideThreads)
+mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
+                const Real* J1, const DecideCand* __restrict__ cand, const DecideHead* __restrict__ head,
+                Ladders lad, EcoTrajRow* rows) {
+    // launched programmatically after the last stage sweep: resident during
+    // its tail, then waits for J_1; the next step's prepare may do the same
+    pdl_launch_dependents();
+    pdl_wait();
+    if (st->status != 0) return;
+    if (threadIdx.x == 0) st->sweep_ns += globaltimer_ns() - st->prep_ns;   // see mpc_prepare_kernel
     const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
     double bestf = 0.0;
     int bestu = -1;
-    // the winner's predicted state and plant-step outputs (v', soc', t',
-    // dt_move, fuel rate, accel) travel with it through the reduction
-    double pred[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (s_src_ok) {
-        for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
-            const int ite = u / c.ntb, itb = u - ite * c.ntb;
-            const double te = c.te_axis[ite], tb = c.tb_axis[itb];
-            if (te > q.te_hi || te < q.te_lo || tb > q.tb_hi || tb < q.tb_lo) continue;
-            const StepOut o = step_eval_pre(P, v, te, tb, r.delta_d, r.accel_min, r.accel_max, 0.0, q);
-            if (o.feas != kFeasOk) continue;
-            if (o.clamped && dst == ECO_NODE_PLAIN) continue;
-            if (dst == ECO_NODE_STOP && o.v_next > 0.0) continue;
-            double cur;
-            if (!battery_current(P, o.p_bat, soc, &cur)) continue;
-            const double soc2 = soc - o.dt_move * cur / P.c_nom;
-            const double t2 = t_base + o.dt_move;
-            if (o.v_next > 0.0) {            // floor-sample green gate mpc.py:256-261
-                int zlo, zhi;
-                double w;
-                if (locate_uniform(t2, lad.t_axis[0], c.dt, c.nt, &zlo, &zhi, &w) && lad.green[c.nt + zlo] == 0)
-                    continue;
-            }
-            const double jn = table_interp<Real>(J1, v1, c.nv, c.soc_axis, c.nx, lad.t_axis, c.nt, c.j_inf,
-                                                 o.v_next, soc2, t2);
-            if (!(jn < c.j_inf)) continue;
-            const double f = stage_cost(o.mf, o.dt_move, c.gamma) + (1.0 - c.gamma) * wait + jn;
-            if (bestu < 0 || f < bestf) {
-                bestf = f; bestu = u;
-                pred[0] = o.v_next; pred[1] = soc2; pred[2] = t2;    // the solver's predicted next state
-                pred[3] = o.dt_move; pred[4] = o.mf; pred[5] = o.accel;
-            }
-        }
+    for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
+        const DecideCand* k = cand + u;
+        if (k->ok == 0.0) continue;
+        const double jn = table_interp<Real>(J1, v1, c.nv, c.soc_axis, c.nx, lad.t_axis, c.nt, c.j_inf, k->v2,
+                                             k->soc2, k->t2);
+        if (!(jn < c.j_inf)) continue;
+        const double f = k->pre + jn;
+        if (bestu < 0 || f < bestf) { bestf = f; bestu = u; }
     }
-    // lexicographic (f, u) min == first win in scan order (mpc.py:269); the
-    // winner's predicted state travels with it (no re-evaluation afterwards)
     for (int o = 16; o > 0; o >>= 1) {
         const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
         const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
-        double p2[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) p2[i] = __shfl_down_sync(0xffffffffu, pred[i], o);
-        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) {
-            bestf = f2; bestu = u2;
-#pragma unroll
-            for (int i = 0; i < 6; ++i) pred[i] = p2[i];
-        }
+        if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
     }
-    __shared__ double s_pred[kDecideThreads / 32][6];
-    if ((threadIdx.x & 31) == 0) {
-        s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) s_pred[threadIdx.x >> 5][i] = pred[i];
-    }
+    __shared__ double s_f[kDecideThreads / 32];
+    __shared__ int s_u[kDecideThreads / 32];
+    const int nw = (int)(blockDim.x >> 5), lane = threadIdx.x & 31;
+    if (lane == 0) { s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu; }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-        const int u2 = s_u[w];
-        const double f2 = s_f[w];
-        if (u2 >= 0 && (bestu < 0 || f2 < bestf || (f2 == bestf && u2 < bestu))) {
-            bestf = f2; bestu = u2;
-#pragma unroll
-            for (int i = 0; i < 6; ++i) pred[i] = s_pred[w][i];
-        }
+    if (threadIdx.x >= 32) return;
+    bestf = lane < nw ? s_f[lane] : 0.0;
+    bestu = lane < nw ? s_u[lane] : -1;
+    for (int o = 16; o > 0; o >>= 1) {
+        const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
+        const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
+        if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
     }
+    if (threadIdx.x != 0) return;
+    const double v = st->x[0], soc = st->x[1], t = st->x[2];
+    const int src = r.kinds[s], dst = r.kinds[s + 1];
     EcoTrajRow row{};
     row.s = s; row.v = v; row.soc = soc; row.t = t; row.horizon = h;
-    double te = 0.0, tb = 0.0, brake = 0.0;
     if (bestu >= 0) {
-        // propagate_state_full (plant.py:341-439) of an admissible winner is
-        // its candidate evaluation: the same step_eval arithmetic with brake
-        // 0 (the comfort box only gates feasibility, which it passed), the
-        // same battery current, the same wait / departure clock -- so the
-        // plant step is the prediction exactly (mpc.py:575-582 holds by
-        // construction) and is not re-run here
-        te = c.te_axis[bestu / c.ntb];
-        tb = c.tb_axis[bestu % c.ntb];
+        // the winner's candidate evaluation is its plant step (see above)
+        const DecideCand* k = cand + bestu;
         row.cost_to_go = bestf;
-        row.t_eng = te; row.t_bsg = tb; row.brake_force = 0.0;
-        row.gear = q.d.gear;
-        row.wait_s = wait; row.dt_move_s = pred[3]; row.fuel_inc_g = pred[4] * pred[3]; row.accel = pred[5];
+        row.t_eng = c.te_axis[bestu / c.ntb]; row.t_bsg = c.tb_axis[bestu % c.ntb]; row.brake_force = 0.0;
+        row.gear = head->gear;
+        row.wait_s = head->wait; row.dt_move_s = k->dt_move; row.fuel_inc_g = k->mf * k->dt_move;
+        row.accel = k->accel;
         rows[st->n_rows] = row;
         st->n_rows += 1;
-        st->x[0] = pred[0]; st->x[1] = pred[1]; st->x[2] = pred[2];
+        st->x[0] = k->v2; st->x[1] = k->soc2; st->x[2] = k->t2;
         return;
-    } else {
-        // _max_braking_decision mpc.py:490-510
-        if (v <= 0.0) { st->status = ECO_RUN_INFEASIBLE; st->status_node = s; return; }
-        double a_target;
-        if (dst == ECO_NODE_PLAIN) {
-            const double a_stop = -(v * v) / (2.0 * r.delta_d) * (1.0 - 1.0e-2);
-            a_target = r.accel_min >= a_stop ? r.accel_min : a_stop;
-        } else {
-            a_target = r.accel_min;
-        }
-        const double f_road = road_load(P, v, r.cos_g[s], r.sin_g[s]);
-        const double b = -(P.mass * a_target + f_road);
-        brake = b > 0.0 ? b : 0.0;
-        row.cost_to_go = __longlong_as_double(0x7ff8000000000000ULL);   // NaN (ControlDecision default)
-        row.fallback = 1;
     }
-    // propagate_state_full plant.py:341-439
+    // _max_braking_decision mpc.py:490-510, then propagate_state_full (rare path)
+    const EcoPlant& P = *plant;
+    const StepPre q = step_pre(P, v, r.cos_g[s], r.sin_g[s]);
+    if (v <= 0.0) { st->status = ECO_RUN_INFEASIBLE; st->status_node = s; return; }
+    double a_target;
+    if (dst == ECO_NODE_PLAIN) {
+        const double a_stop = -(v * v) / (2.0 * r.delta_d) * (1.0 - 1.0e-2);
+        a_target = r.accel_min >= a_stop ? r.accel_min : a_stop;
+    } else {
+        a_target = r.accel_min;
+    }
+    const double f_road = road_load(P, v, r.cos_g[s], r.sin_g[s]);
+    const double b = -(P.mass * a_target + f_road);
+    const double brake = b > 0.0 ? b : 0.0;
+    row.cost_to_go = __longlong_as_double(0x7ff8000000000000ULL);   // NaN (ControlDecision default)
+    row.fallback = 1;
+    const double te = 0.0, tb = 0.0;
     if (!(q.te_lo <= te && te <= q.te_hi) || !(q.tb_lo <= tb && tb <= q.tb_hi) || brake < 0.0) {
         st->status = ECO_RUN_PLANT; st->status_node = s; return;
     }
@@ -370,13 +405,12 @@ mpc_decide_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, Loo
     }
     double cur;
     if (!battery_current(P, o.p_bat, soc, &cur)) { st->status = ECO_RUN_PLANT; st->status_node = s; return; }
-    const double nx0 = o.v_next, nx1 = soc - o.dt_move * cur / P.c_nom, nx2 = tb_p + o.dt_move;
     row.t_eng = te; row.t_bsg = tb; row.brake_force = brake;
     row.gear = q.d.gear;
     row.wait_s = wait_p; row.dt_move_s = o.dt_move; row.fuel_inc_g = o.mf * o.dt_move; row.accel = o.accel;
     rows[st->n_rows] = row;
     st->n_rows += 1;
-    st->x[0] = nx0; st->x[1] = nx1; st->x[2] = nx2;
+    st->x[0] = o.v_next; st->x[1] = soc - o.dt_move * cur / P.c_nom; st->x[2] = tb_p + o.dt_move;
 }
 
 // Batch scenarios (C4): per scenario b the time ladder at t_start[b]

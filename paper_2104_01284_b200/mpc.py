@@ -234,7 +234,9 @@ class MpcSession:
 
     def run(self, x_start: StateVector, start_node: int = 0, max_steps: int = -1, *, count_live: bool = False,
             time_sweeps: bool = True):
-        """Closed loop on the device -> (rows, status, status_node, final_state, stats)."""
+        """Closed loop on the device -> (rows, status, status_node, final_state, stats).
+        ``stats["dominant_ms"]`` is the summed per-step solve clock (device
+        timestamps, always on; ``time_sweeps`` is accepted and ignored)."""
         rows = np.zeros(max(self.route.node_count - 1, 1), dtype=_abi.TRAJ_DTYPE)
         x0 = np.array([x_start.v, x_start.soc, x_start.t], dtype=np.float64)
         fin = np.zeros(3)
