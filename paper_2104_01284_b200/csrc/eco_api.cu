@@ -325,9 +325,21 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     const int light = light_first<Real>(G, g.nt, (phi - G.plo) * G.nchunk);
     geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, phi, light, G.order.p, G.rank_of.p);
     ECO_CUDA(cudaGetLastError());
-    dim3 tgrid(g.nv * G.nchunk, g.P);
-    geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
-        G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
+    // one block per (plan, plane) covering all its SoC chunks (coalesced row
+    // records); the per-tile kernel remains for grids whose chunk tables
+    // exceed shared memory
+    const size_t psmem = ((size_t)3 * G.nchunk * g.nv + G.nchunk) * sizeof(int32_t);
+    if (psmem <= 200 * 1024 && env_int("ECO_PLANE_TILES", 1) != 0) {
+        if (psmem > 48 * 1024)
+            ECO_CUDA(cudaFuncSetAttribute(geom_plane_tiles_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)psmem));
+        geom_plane_tiles_kernel<Real><<<dim3(g.nv, g.P), 256, psmem, st>>>(
+            G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
+    } else {
+        dim3 tgrid(g.nv * G.nchunk, g.P);
+        geom_tiles_kernel<Real><<<tgrid, 256, (size_t)g.nv * 2 * sizeof(int32_t), st>>>(
+            G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
+    }
     ECO_CUDA(cudaGetLastError());
     if (launches) *launches += 6;
 }

@@ -351,6 +351,100 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
     }
 }
 
+// The same per-tile plans and row records, one block per (plan, source
+// plane) for all of the plane's SoC chunks: the plane's row records are read
+// and written contiguously (coalesced) and the chunk headers are built in
+// parallel (one thread per chunk).  grid (nv, P), block 256, dyn smem
+// 3 * nchunk * nv ints + nchunk ints.
+template <typename Real>
+__global__ void __launch_bounds__(256)
+geom_plane_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap,
+                        TilePlan* __restrict__ tiles, RowRec2<Real>* __restrict__ row2,
+                        const int32_t* __restrict__ rank_of, const DevPlan* __restrict__ plans,
+                        const double* __restrict__ vaxes) {
+    extern __shared__ int32_t s_dyn[];
+    const int nv = d.nv, nx = d.nx;
+    int32_t* s_lo = s_dyn;                           // [nchunk][nv]
+    int32_t* s_hi = s_lo + nchunk * nv;              // [nchunk][nv]
+    int32_t* s_segof = s_hi + nchunk * nv;           // [nchunk][nv]
+    int32_t* s_ok = s_segof + nchunk * nv;           // [nchunk]
+    const int p = blockIdx.y, iv = blockIdx.x;
+    const size_t pi = (size_t)p * nv + iv;
+    const int n = g.count[pi];
+    const int64_t roff = g.row_off[pi];
+    const RowRec<Real>* rows = g.row + roff;
+    const ActRec<Real>* acts = g.act + pi * d.U;
+    for (int q = threadIdx.x; q < nchunk * nv; q += blockDim.x) { s_lo[q] = nx; s_hi[q] = -1; }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * nx; i += blockDim.x) {
+        const RowRec<Real> ro = rows[i];
+        if (ro.off < 0) continue;
+        const int k = i / nx, c = (i - k * nx) / tj;
+        const int dlo = ro.cell / nx, jl = ro.cell - dlo * nx;
+        const int jh = jl + (ro.wx > (Real)0 ? 1 : 0);
+        const int dhi = dlo + ((acts[k].meta & kRecDvh) ? 1 : 0);
+        int32_t* lo = s_lo + c * nv;
+        int32_t* hi = s_hi + c * nv;
+        atomicMin(&lo[dlo], jl); atomicMax(&hi[dlo], jh);
+        if (dhi != dlo) { atomicMin(&lo[dhi], jl); atomicMax(&hi[dhi], jh); }
+    }
+    __syncthreads();
+    const size_t tbase = (size_t)p * nv * nchunk;
+    for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
+        const int j0 = c * tj, tja = min(tj, nx - j0);
+        TilePlan* tp = tiles + tbase + rank_of[tbase + (size_t)iv * nchunk + c];
+        const double v = vaxes[(size_t)p * nv + iv];
+        tp->iv = iv;
+        tp->j0 = j0;
+        tp->tja = tja;
+        tp->count = (plans[p].src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : n;   // K:458-459
+        tp->moving = v > 0.0;
+        tp->row_off = roff;
+        const int32_t* lo = s_lo + c * nv;
+        const int32_t* hi = s_hi + c * nv;
+        int32_t* segof = s_segof + c * nv;
+        int ns = 0, run = 0, ok = 1;
+        for (int q = 0; q < nv && ok; ++q) {
+            segof[q] = -1;
+            if (hi[q] < lo[q]) continue;
+            if (ns == kMaxSeg) { ok = 0; break; }
+            const int len = (hi[q] - lo[q] + 1) * d.nt;
+            segof[q] = run;
+            tp->gofs[ns] = (q * nx + lo[q]) * d.nt;
+            tp->len[ns] = len;
+            tp->sofs[ns] = run;
+            run += len;
+            ++ns;
+        }
+        if (run > band_cap) ok = 0;
+        tp->nseg = ok ? ns : -1;
+        tp->band = ok ? run : 0;
+        s_ok[c] = ok;
+    }
+    __syncthreads();
+    RowRec2<Real>* out = row2 + roff;
+    for (int i = threadIdx.x; i < n * nx; i += blockDim.x) {
+        const int k = i / nx, jx = i - k * nx, c = jx / tj;
+        if (!s_ok[c]) continue;                       // L1-path tile: no row records
+        const RowRec<Real> ro = rows[i];
+        RowRec2<Real> q;
+        q.blo = 0; q.bhi = 0; q.zlim = -1; q.wx = (Real)0;
+        if (ro.off >= 0) {
+            const ActRec<Real> ac = acts[k];
+            const int zoff = (int)(ac.meta & kRecZoff);
+            const int dlo = ro.cell / nx, jl = ro.cell - dlo * nx;
+            const int dhi = dlo + ((ac.meta & kRecDvh) ? 1 : 0);
+            const int32_t* lo = s_lo + c * nv;
+            const int32_t* segof = s_segof + c * nv;
+            q.blo = segof[dlo] + (jl - lo[dlo]) * d.nt + zoff;
+            q.bhi = segof[dhi] + (jl - lo[dhi]) * d.nt + zoff;
+            q.zlim = ro.zlim;
+            q.wx = ro.wx;
+        }
+        out[i] = q;
+    }
+}
+
 // per plan: tiles heaviest first -- planes by descending feasible-action
 // count (ties by plane index), the SoC chunks of a plane consecutively.  The
 // order only balances the load; results do not depend on it.
