@@ -222,7 +222,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     h2d = mpc.upload_bytes_ + 3 * 8          # route / SPaT arrays re-sent by every fit + x0
-    d2h = traj.n_steps * 120 + 3 * 8 + mpc.terminal_field_.values.nbytes + 4 * 3
+    d2h = traj.n_steps * (120 + 8) + 3 * 8 + mpc.terminal_field_.values.nbytes + 4 * 3   # rows + step clocks
 
     if rank != 0:
         if dist is not None:

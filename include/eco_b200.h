@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECO_ABI_VERSION 4
+#define ECO_ABI_VERSION 5
 
 #define ECO_MAX_GEARS 16
 #define ECO_MAX_AXIS 32
@@ -255,6 +255,10 @@ int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,
                         const double* x_start, EcoTrajRow* rows, int32_t* n_rows,
                         int32_t* status, int32_t* status_node,
                         double* final_state, int32_t flags, EcoStats* stats);
+/* per-step solve clocks (ms, device timestamps: context preparation entry ->
+ * decision entry) of the last eco_session_run's first n steps (n <= the
+ * steps that run took). */
+int32_t eco_session_step_times(EcoSession* sess, double* solve_ms, int32_t n);
 int32_t eco_session_destroy(EcoSession* sess);
 
 /* Phase plan of one signal (SignalTiming route.py:50-86): green windows

@@ -21,7 +21,7 @@ MAX_GEARS = 16
 MAX_AXIS = 32
 MAX_MAP = MAX_AXIS * MAX_AXIS
 MAX_WINDOWS = 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 XCHG_P2P, XCHG_NCCL = 0, 1
 SLAB_INFO_BYTES = 256
 
@@ -237,6 +237,7 @@ def _declare(lib):
         "eco_session_fit": (_I, [C.c_void_p, _PD, _PD, P(EcoStats)]),
         "eco_session_upload_route": (_I, [C.c_void_p, P(EcoRoute)]),
         "eco_session_run": (_I, [C.c_void_p, _I, _I, _PD, P(EcoTrajRow), _PI, _PI, _PI, _PD, _I, P(EcoStats)]),
+        "eco_session_step_times": (_I, [C.c_void_p, _PD, _I]),
         "eco_session_destroy": (_I, [C.c_void_p]),
         "eco_batch_create": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), P(C.c_void_p)]),
         "eco_batch_solve": (_I, [C.c_void_p, _I, C.c_void_p, _PI, _PD, _PD, _PI, _I, P(EcoStats)]),

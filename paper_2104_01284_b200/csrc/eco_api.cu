@@ -1164,6 +1164,7 @@ struct SessionBase {
     virtual void fit(const double* field_in, double* field_out, EcoStats* stats) = 0;
     virtual void run(int start_node, int max_steps, const double* x0, EcoTrajRow* rows, int32_t* n_rows,
                      int32_t* status, int32_t* status_node, double* final_state, int flags, EcoStats* stats) = 0;
+    virtual void step_times(double* out_ms, int n) = 0;
 };
 
 constexpr int kRunCountLive = 1;
@@ -1180,6 +1181,8 @@ struct Session : SessionBase {
     DBuf<Real> field_int;          // internal (n, nv, nx)
     bool fitted = false;
     DBuf<LoopState> state;
+    DBuf<unsigned long long> step_ns;   // per-step solve clocks of the last run
+    int last_rows = 0;
     DBuf<DecideCand> dec_cand;      // split decide: per-action candidate records
     DBuf<DecideHead> dec_head;
     cudaStream_t dec_side = nullptr;
@@ -1232,6 +1235,14 @@ struct Session : SessionBase {
         if (dec_join) cudaEventDestroy(dec_join);
         if (dec_side) cudaStreamDestroy(dec_side);
         if (st) cudaStreamDestroy(st);
+    }
+
+    void step_times(double* out_ms, int n_req) override {
+        if (n_req < 0 || n_req > last_rows) throw ArgError{"more step times requested than the last run took"};
+        std::vector<unsigned long long> h((size_t)n_req);
+        if (n_req) step_ns.download(h.data(), (size_t)n_req, st);
+        ECO_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < n_req; ++i) out_ms[i] = (double)h[i] * 1e-6;
     }
 
     void upload_route(const EcoRoute* r) override {
@@ -1302,6 +1313,7 @@ struct Session : SessionBase {
         }
         dec_cand.ensure((size_t)U);
         dec_head.ensure(1);
+        step_ns.ensure((size_t)n);
         int64_t stages = 0;
         auto enqueue = [&](cudaStream_t qs) {
             stages = 0;
@@ -1367,7 +1379,7 @@ struct Session : SessionBase {
                 ECO_CUDA(cudaStreamWaitEvent(qs, dec_join, 0));
                 launch_pdl(mpc_pick_kernel<Real>, 1, std::min(kDecideThreads, (U + 31) / 32 * 32), qs, true,
                            (const EcoPlant*)ctx.plant.p, ctx.R.view, lc, state.p, s, h, (const Real*)(J.p + LV),
-                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p);
+                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p, step_ns.p);
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
             }
@@ -1409,6 +1421,7 @@ struct Session : SessionBase {
         rows.download(out_rows, hs.n_rows, st);
         ECO_CUDA(cudaStreamSynchronize(st));
         *n_rows = hs.n_rows;
+        last_rows = hs.n_rows;
         *status = hs.status;
         *status_node = hs.status_node;
         final_state[0] = hs.x[0]; final_state[1] = hs.x[1]; final_state[2] = hs.x[2];
@@ -2012,6 +2025,13 @@ int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,
             throw ArgError{"null pointer argument"};
         reinterpret_cast<SessionBase*>(sess)->run(start_node, max_steps, x_start, rows, n_rows, status, status_node,
                                                   final_state, flags, stats);
+    });
+}
+
+int32_t eco_session_step_times(EcoSession* sess, double* solve_ms, int32_t n) {
+    return run_guarded([&] {
+        if (!sess || (n > 0 && !solve_ms)) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SessionBase*>(sess)->step_times(solve_ms, n);
     });
 }
 

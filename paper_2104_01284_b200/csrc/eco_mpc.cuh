@@ -310,13 +310,17 @@ template <typename Real>
 __global__ void __launch_bounds__(kDecideThreads)
 mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
                 const Real* J1, const DecideCand* __restrict__ cand, const DecideHead* __restrict__ head,
-                Ladders lad, EcoTrajRow* rows) {
+                Ladders lad, EcoTrajRow* rows, unsigned long long* step_ns) {
     // launched programmatically after the last stage sweep: resident during
     // its tail, then waits for J_1; the next step's prepare may do the same
     pdl_launch_dependents();
     pdl_wait();
     if (st->status != 0) return;
-    if (threadIdx.x == 0) st->sweep_ns += globaltimer_ns() - st->prep_ns;   // see mpc_prepare_kernel
+    if (threadIdx.x == 0) {                      // per-step solve clock (see mpc_prepare_kernel)
+        const unsigned long long dt = globaltimer_ns() - st->prep_ns;
+        st->sweep_ns += dt;
+        step_ns[st->n_rows] = dt;
+    }
     const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
     double bestf = 0.0;
     int bestu = -1;

@@ -249,6 +249,14 @@ class MpcSession:
             _abi.ptr(fin, C.c_double), flags, C.byref(st)), "eco_session_run")
         return rows[:n_rows.value], status.value, node.value, fin, st.as_dict()
 
+    def step_times(self, n: int) -> np.ndarray:
+        """Per-step solve clocks (s) of the last :meth:`run`'s first n steps:
+        device timestamps from context preparation to the decision."""
+        out = np.zeros(max(n, 0))
+        _abi.check(self._lib.eco_session_step_times(self._h, _abi.ptr(out, C.c_double), n),
+                   "eco_session_step_times")
+        return out * 1e-3
+
     def close(self):
         if self._h:
             self._lib.eco_session_destroy(self._h)
@@ -401,7 +409,8 @@ class EcoDrivingMPC:
         r = rows[0]
         return ControlDecision(action=ActionVector(t_eng=float(r["t_eng"]), t_bsg=float(r["t_bsg"])),
                                predicted_next=StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2])),
-                               cost_to_go=float(r["cost_to_go"]), solver_wall_s=st["device_ms"] / 1e3)
+                               cost_to_go=float(r["cost_to_go"]),
+                               solver_wall_s=float(self.session_.step_times(1)[0]))
 
     def _check_fitted(self):
         if not hasattr(self, "route_"):
@@ -436,8 +445,7 @@ def simulate_closed_loop(route: Route, spat: SpatSchedule, controller: EcoDrivin
     if status == _abi.RUN_MISMATCH:
         raise RuntimeError(f"solver/plant transition mismatch at node {node}")
     traj.steps = _rows_to_steps(rows)
-    per = st["dominant_ms"] / 1e3 / max(len(rows), 1)
-    traj.solver_wall_s = [per] * len(rows)
+    traj.solver_wall_s = [float(x) for x in controller.session_.step_times(len(rows))]
     traj.final_state = StateVector(v=float(fin[0]), soc=float(fin[1]), t=float(fin[2]))
     if status != _abi.RUN_OK:
         traj.status = _STATUS_TEXT[status].format(node=node)

@@ -510,3 +510,15 @@ def test_c4_full_batch_fp32_vs_fp64(vehicle):
         r32 = b.solve(None, sched, timings=tim)
     mask, p999, mx, pol = fp32_agreement(r32.J0, r32.P0, r64.J0, r64.P0)
     assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (mask, p999, mx, pol)
+
+
+def test_closed_loop_step_clocks(vehicle, short_route):
+    """Per-step solve clocks (device timestamps) behind the timing CSV."""
+    route, spat = short_route
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=SMALL, penalty=PEN, horizon=8, backend="b200").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    w = np.asarray(traj.solver_wall_s)
+    assert w.shape == (traj.n_steps,) and np.all(w > 0) and np.all(w < 0.05)
+    assert abs(w.sum() * 1e3 - traj.stats["dominant_ms"]) <= 1e-6 * max(1.0, traj.stats["dominant_ms"])
+    dec = mpc.control(StateVector(v=5.0, soc=0.5, t=0.0), 3)
+    assert 0 < dec.solver_wall_s < 0.05
