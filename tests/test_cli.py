@@ -51,13 +51,14 @@ def test_cli_run_diff_bench(tmp_path, capsys):
     out = tmp_path / "out"
     base = ["--route", "short", "--seed", "2", "--config", str(cfg), "--out", str(out)]
     assert main(["run", "--backend", "b200-fp64"] + base) == EXIT_OK
-    for name in ("trajectory_mpc_short.csv", "timing_mpc_short.csv", "summary_short.json"):
-        assert (out / name).is_file()
-    summary = json.loads((out / "summary_short.json").read_text())
+    name = "short-1p2km"                           # the fixture route's name
+    for f in (f"trajectory_mpc_{name}.csv", f"timing_mpc_{name}.csv", f"summary_{name}.json"):
+        assert (out / f).is_file()
+    summary = json.loads((out / f"summary_{name}.json").read_text())
     assert summary["runs"]["mpc"]["status"] == "ok" and summary["backend"] == "b200-fp64"
     assert main(["diff-backends", "--backend", "b200-fp64", "--against", "b200-fp64"] + base) == EXIT_OK
     assert "policy mismatches total: 0" in capsys.readouterr().out
     assert main(["bench", "--reps", "30", "--warmup", "2"] + base) == EXIT_OK
     txt = capsys.readouterr().out
     assert "b200-fp64" in txt and "speedup (b200 mean / b200-fp64 mean)" in txt
-    assert (out / "bench_short.csv").is_file()
+    assert (out / f"bench_{name}.csv").is_file() and (out / f"diff_backends_{name}.csv").is_file()
