@@ -447,7 +447,15 @@ void set_smem_attr(K kernel, size_t smem) {
     done.emplace_back((const void*)kernel, smem);
 }
 
-inline int sm_count_cached();
+inline int sm_count_cached() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        ECO_CUDA(cudaGetDevice(&dev));
+        ECO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
 
 // Tiles a stage launch puts in front (geom_order_kernel): when the launch is
 // between one and two waves of resident CTAs, the overflow count.
@@ -504,67 +512,6 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
         ECO_CUDA(cudaLaunchKernelEx(&lc, field_stage_kernel<Real>, a));
     }
     ECO_CUDA(cudaGetLastError());
-}
-
-// Cooperative persistent launch of all stages of a solve (bellman_solve_kernel).
-struct SolveSync {
-    DBuf<unsigned> bar;
-    DBuf<int> tile_ctr;
-    void ensure(int H) {
-        if (!bar.p) {
-            bar.alloc(2);
-            ECO_CUDA(cudaMemset(bar.p, 0, 2 * sizeof(unsigned)));
-        }
-        if (tile_ctr.n < (size_t)H) tile_ctr.alloc(H);
-    }
-};
-
-inline int sm_count_cached() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        ECO_CUDA(cudaGetDevice(&dev));
-        ECO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return n;
-}
-
-inline int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        ECO_CUDA(cudaGetDevice(&dev));
-        ECO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return n;
-}
-
-template <typename Real>
-void launch_solve(SolveArgs<Real>& sa, const TileCfg& tc, bool count, SolveSync& sync, cudaStream_t st) {
-    sync.ensure(sa.H);
-    sa.bar = sync.bar.p;
-    sa.tile_ctr = sync.tile_ctr.p;
-    ECO_CUDA(cudaMemsetAsync(sync.tile_ctr.p, 0, sa.H * sizeof(int), st));
-    const int block = tc.S * tc.slices;
-    auto k = count ? bellman_solve_kernel<Real, true> : bellman_solve_kernel<Real, false>;
-    set_smem_attr(k, tc.smem);
-    int per_sm = 0;
-    ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, tc.smem));
-    if (per_sm < 1) throw ArgError{"solve kernel does not fit on an SM"};
-    const int grid = std::min(per_sm * sm_count(), std::max(1, sa.ntiles));
-    void* args[] = {&sa};
-    ECO_CUDA(cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(block), args, tc.smem, st));
-}
-
-template <typename Real>
-SolveArgs<Real> solve_args(Geometry<Real>& G, const TileCfg& tc, int nt) {
-    SolveArgs<Real> sa{};
-    sa.base = stage_args(G, 0, nullptr, nt, tc);
-    sa.pair_stride = (size_t)G.dims.nv * G.dims.U;
-    sa.plane_stride = G.dims.nv;
-    sa.tile_stride = G.dims.nv * G.nchunk;
-    sa.ntiles = G.dims.nv * G.nchunk;
-    return sa;
 }
 
 void check_problem(const EcoProblem* pr) {
@@ -779,13 +726,10 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     }
     std::vector<TileCfg> tcs(H);
     for (int k = 0; k < H; ++k) tcs[k] = tile_cfg(tabs ? toyG[k] : G, nt, 0);
-    SolveSync ssync;
-    const bool persistent = !tabs && env_int("ECO_PERSISTENT", 0) != 0 && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
-                            !tcs[0].wide;
     // large outputs (fine grids): overlap each level's D2H with the later
     // stages.  Small stacks go in one copy at the end: per-level pageable
     // copies cost more than they hide (C2: 1.67 vs 1.16 ms per solve call)
-    const bool overlap = !tabs && !persistent && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
+    const bool overlap = !tabs && env_int("ECO_DEBUG_STAGE", 0) == 0 &&
                          ns * (size_t)(H + 1) * sizeof(double) > (size_t(256) << 20);
     static cudaStream_t ovs = nullptr;
     static std::vector<cudaEvent_t> lvl_ev;
@@ -799,54 +743,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         ECO_CUDA(cudaEventRecord(lvl_ev[H], st));       // the terminal level is in place
     }
     sweep.start(st);
-    if (persistent) {
-        SolveArgs<Real> sa = solve_args(G, tcs[0], nt);
-        sa.base.live = count ? d_live.p : nullptr;
-        sa.base.t0 = pr->t0;
-        sa.base.dtg = pr->dtg;
-        sa.base.j_inf = (Real)pr->j_inf;
-        sa.vaxes = in.v;
-        sa.src_kinds = in.kinds;
-        sa.plan0 = 0;
-        sa.H = H;
-        sa.green_shift = 0;
-        sa.green = in.green; sa.dep_ok = in.dep; sa.t_dep = in.tdep; sa.wait = in.wait;
-        sa.J = d_J.p; sa.LV = LV; sa.LC = LC;
-        sa.P = d_P.p; sa.PV = ns;
-        DBuf<unsigned long long> dbgbuf;
-        const bool dbg_on = env_int("ECO_DEBUG_SOLVE", 0) != 0;
-        if (dbg_on) {
-            dbgbuf.alloc((size_t)4 * H * 2048);
-            ECO_CUDA(cudaMemsetAsync(dbgbuf.p, 0, dbgbuf.n * 8, st));
-            sa.base.dbg = dbgbuf.p;
-        }
-        launch_solve(sa, tcs[0], count, ssync, st);
-        ++launches;
-        if (dbg_on) {
-            std::vector<unsigned long long> h(dbgbuf.n);
-            dbgbuf.download(h.data(), h.size(), st);
-            ECO_CUDA(cudaStreamSynchronize(st));
-            int nb = 0;
-            while (nb < 2048 && h[(size_t)nb * 4 * H + 4 * (H - 1)]) ++nb;
-            unsigned long long t0 = ~0ull;
-            for (int b = 0; b < nb; ++b) t0 = std::min(t0, h[(size_t)b * 4 * H + 4 * (H - 1)]);
-            for (int k = H - 1; k >= 0; --k) {
-                double s0 = 1e30, e_min = 1e30, e_max = 0, b_max = 0, nt_max = 0, nt_min = 1e9;
-                for (int b = 0; b < nb; ++b) {
-                    const unsigned long long* d = &h[(size_t)b * 4 * H + 4 * k];
-                    s0 = std::min(s0, (d[0] - t0) / 1e3);
-                    const double e = (d[1] - t0) / 1e3;
-                    e_min = std::min(e_min, e); e_max = std::max(e_max, e);
-                    if (d[2]) b_max = std::max(b_max, (d[2] - t0) / 1e3);
-                    nt_max = std::max(nt_max, (double)d[3]); nt_min = std::min(nt_min, (double)d[3]);
-                }
-                std::fprintf(stderr, "stage %2d start %8.2f tiles-done min %8.2f max %8.2f barrier-out %8.2f tiles/cta %.0f..%.0f\n",
-                             k, s0, e_min, e_max, b_max, nt_min, nt_max);
-            }
-            std::fprintf(stderr, "grid %d ctas\n", nb);
-        }
-    }
-    for (int k = H - 1; k >= 0 && !persistent; --k) {
+    for (int k = H - 1; k >= 0; --k) {
         const TileCfg& tc = tcs[k];
         StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, in.v + (size_t)k * nv, nt, tc)
                                  : stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
@@ -1194,7 +1091,6 @@ struct Session : SessionBase {
     DBuf<int32_t> P;
     DBuf<EcoTrajRow> rows;
     DBuf<unsigned long long> live;
-    SolveSync ssync;
     cudaStream_t st = 0;
     // CUDA graph of a whole closed loop (prepare / H stage sweeps / decide per
     // node), captured on first use and replayed: no per-kernel launch gaps
@@ -1305,7 +1201,6 @@ struct Session : SessionBase {
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
         const TileCfg tc = tile_cfg(ctx.G, nt, 0);
-        const bool persistent = env_int("ECO_PERSISTENT", 0) != 0 && !tc.wide;
         if (!dec_side) {
             ECO_CUDA(cudaStreamCreateWithFlags(&dec_side, cudaStreamNonBlocking));
             ECO_CUDA(cudaEventCreateWithFlags(&dec_fork, cudaEventDisableTiming));
@@ -1335,26 +1230,7 @@ struct Session : SessionBase {
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
                 ECO_CUDA(cudaEventRecord(dec_join, dec_side));
-                if (persistent) {
-                    SolveArgs<Real> sa = solve_args(ctx.G, tc, nt);
-                    sa.base.status = &state.p->status;
-                    sa.base.live = count ? live.p : nullptr;
-                    sa.base.t0_dev = tax.p;
-                    sa.base.dtg = cfg.dt;
-                    sa.base.j_inf = (Real)cfg.j_inf;
-                    sa.vaxes = ctx.R.vaxes.p;
-                    sa.src_kinds = ctx.R.kinds.p;
-                    sa.plan0 = s;
-                    sa.H = h;
-                    sa.green_shift = 1;
-                    sa.green = green.p; sa.dep_ok = dep.p; sa.t_dep = tdep.p; sa.wait = wait.p;
-                    sa.J = J.p; sa.LV = LV; sa.LC = LC;
-                    sa.P = P.p; sa.PV = 0;
-                    launch_solve(sa, tc, count, ssync, qs);
-                    ++launches;
-                    stages += h;
-                }
-                for (int k = h - 1; k >= 0 && !persistent; --k) {
+                for (int k = h - 1; k >= 0; --k) {
                     StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tc);
                     a.green = green.p + (size_t)(k + 1) * nt;
                     a.dep_ok = dep.p + (size_t)k * nt;
@@ -1384,7 +1260,7 @@ struct Session : SessionBase {
                 ++launches;
             }
         };
-        const bool use_graph = !count && !persistent && env_int("ECO_GRAPH", 1) != 0;
+        const bool use_graph = !count && env_int("ECO_GRAPH", 1) != 0;
         if (use_graph) {
             const std::vector<long long> key = {start_node, s_end, (long long)(size_t)ctx.G.row2.p,
                                                 (long long)(size_t)ctx.G.tiles.p, (long long)(size_t)ctx.G.order.p,

@@ -1388,108 +1388,3 @@ field_stage_kernel(StageArgs<Real> a) {
 }
 
 }  // namespace eco
-
-namespace eco {
-
-// =====================================================================
-// Persistent horizon solve (K2): one cooperative launch runs all H Bellman
-// stages (solve_horizon's loop dp.py:446-450) with a grid barrier between
-// consecutive stages; CTAs pull tiles of the current stage heaviest-first
-// from an atomic counter, so no launch gap sits between stages and the
-// per-stage load imbalance is absorbed dynamically.
-// =====================================================================
-template <typename Real>
-struct SolveArgs {
-    StageArgs<Real> base;         // plan-0 geometry pointers, dims, tile shape, scalars
-    size_t pair_stride;           // nv * U      (u, dt, c1d, act)
-    int plane_stride;             // nv          (count, row_off)
-    int tile_stride;              // nv * nchunk (tiles, order)
-    const double* vaxes;          // [P][nv] source speed axes
-    const int8_t* src_kinds;      // [P]
-    int plan0, H, ntiles;
-    int green_shift;              // 1: ladders are [H+1][nt] node arrays (stage k reads green k+1)
-    const uint8_t* green;
-    const uint8_t* dep_ok;
-    const double* t_dep;
-    const double* wait;
-    Real* J;                      // level k at J + k * LV (copy 0) and + LC (copy 1)
-    size_t LV, LC;
-    int32_t* P;                   // level k at P + k * PV
-    size_t PV;
-    unsigned* bar;                // [2]: arrivals, generation
-    int* tile_ctr;                // [H]
-};
-
-// generation barrier over the (co-resident, cooperative-launched) grid
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* vgen = bar + 1;
-        const unsigned gen = *vgen;
-        __threadfence();
-        if (atomicAdd(&bar[0], 1u) == nblocks - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(&bar[1], 1u);
-        } else {
-            while (*vgen == gen) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-template <typename Real>
-__device__ __forceinline__ StageArgs<Real> stage_of(const SolveArgs<Real>& sa, int k) {
-    StageArgs<Real> a = sa.base;
-    const int p = sa.plan0 + k;
-    a.count += (size_t)p * sa.plane_stride;
-    a.row_off += (size_t)p * sa.plane_stride;
-    a.u += (size_t)p * sa.pair_stride;
-    a.dt += (size_t)p * sa.pair_stride;
-    a.c1d += (size_t)p * sa.pair_stride;
-    a.act += (size_t)p * sa.pair_stride;
-    a.tiles += (size_t)p * sa.tile_stride;
-    a.order += (size_t)p * sa.tile_stride;
-    a.v_src = sa.vaxes + (size_t)p * a.nv;
-    a.src_kind = sa.src_kinds[p];
-    a.green = sa.green + (size_t)(k + sa.green_shift) * a.nt;
-    a.dep_ok = sa.dep_ok + (size_t)k * a.nt;
-    a.t_dep = sa.t_dep + (size_t)k * a.nt;
-    a.wait = sa.wait + (size_t)k * a.nt;
-    a.J_next = sa.J + (size_t)(k + 1) * sa.LV;
-    a.J_next1 = a.J_next + sa.LC;
-    a.J_out = sa.J + (size_t)k * sa.LV;
-    a.J_out1 = a.J_out + sa.LC;
-    a.P_out = sa.P + (size_t)k * sa.PV;
-    return a;
-}
-
-template <typename Real, bool COUNT>
-__global__ void __launch_bounds__(512)
-bellman_solve_kernel(SolveArgs<Real> sa) {
-    if (sa.base.status && *sa.base.status != 0) return;    // same value for every CTA
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int s_rank;
-    unsigned long long* dbg = sa.base.dbg ? sa.base.dbg + (size_t)blockIdx.x * 4 * sa.H : nullptr;
-    for (int k = sa.H - 1; k >= 0; --k) {
-        StageArgs<Real> a = stage_of(sa, k);
-        a.dbg = nullptr;
-        int ntile = 0;
-        if (dbg && threadIdx.x == 0) dbg[4 * k] = gtimer();
-        for (;;) {
-            if (threadIdx.x == 0) s_rank = atomicAdd(&sa.tile_ctr[k], 1);
-            __syncthreads();
-            const int rank = s_rank;
-            __syncthreads();
-            if (rank >= sa.ntiles) break;
-            stage_tile<Real, COUNT>(a, rank, smem);
-            ++ntile;
-        }
-        if (dbg && threadIdx.x == 0) { dbg[4 * k + 1] = gtimer(); dbg[4 * k + 3] = ntile; }
-        if (k > 0) grid_barrier(sa.bar, gridDim.x);
-        if (dbg && threadIdx.x == 0) dbg[4 * k + 2] = gtimer();
-    }
-}
-
-}  // namespace eco
