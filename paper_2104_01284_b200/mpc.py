@@ -178,13 +178,16 @@ class ClosedLoopTrajectory:
         return {"mean_ms": float(arr.mean()), "variance_ms2": float(arr.var()), "max_ms": float(arr.max())}
 
 
+_STEP_FIELDS = ("s", "v", "soc", "t", "t_eng", "t_bsg", "brake_force", "gear", "wait_s", "dt_move_s", "fuel_inc_g",
+                "accel", "cost_to_go")
+
+
 def _rows_to_steps(rows: np.ndarray) -> list:
-    return [TrajectoryStep(
-        s=int(r["s"]), v=float(r["v"]), soc=float(r["soc"]), t=float(r["t"]), t_eng=float(r["t_eng"]),
-        t_bsg=float(r["t_bsg"]), brake_force=float(r["brake_force"]), gear=int(r["gear"]),
-        wait_s=float(r["wait_s"]), dt_move_s=float(r["dt_move_s"]), fuel_inc_g=float(r["fuel_inc_g"]),
-        accel=float(r["accel"]), cost_to_go=float(r["cost_to_go"]), fallback=bool(r["fallback"]))
-        for r in rows]
+    # column-wise tolist(): exact Python ints / floats, ~10x faster than
+    # converting row by row (699 rows of a C2 run are in the e2e timing)
+    cols = [rows[f].tolist() for f in _STEP_FIELDS]
+    cols.append([x != 0 for x in rows["fallback"].tolist()])
+    return [TrajectoryStep(*vals) for vals in zip(*cols)]
 
 
 class MpcSession:
