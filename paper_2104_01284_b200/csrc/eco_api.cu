@@ -1116,7 +1116,7 @@ struct Session : SessionBase {
         green.alloc((size_t)(H + 1) * nt); dep.alloc((size_t)(H + 1) * nt);
         tdep.alloc((size_t)(H + 1) * nt); wait.alloc((size_t)(H + 1) * nt); tax.alloc(nt);
         sflags.alloc(H);
-        J.alloc((size_t)(H + 1) * level_stride(ns));
+        J.alloc((size_t)2 * (H + 1) * level_stride(ns));   // two stacks, alternating by step
         P.alloc(ns);
         rows.alloc(n - 1);
         live.alloc(1);
@@ -1213,22 +1213,38 @@ struct Session : SessionBase {
         auto enqueue = [&](cudaStream_t qs) {
             stages = 0;
             launches = 0;
+            const size_t LV = level_stride(ns), LC = level_copy(ns);
+            const int seed_grid = std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256));
+            const double* fld = cfg.use_terminal_field ? (const double*)field.p : nullptr;
+            // two J stacks, alternating by step: step s + 1's terminal level is
+            // seeded on the side branch while step s still sweeps its own
+            auto Jstack = [&](int s) { return J.p + (size_t)((s - start_node) & 1) * (H + 1) * LV; };
+            auto horizon = [&](int s) { return H < n - 1 - s ? H : n - 1 - s; };
             for (int s = start_node; s < s_end; ++s) {
-                const int h = H < n - 1 - s ? H : n - 1 - s;
-                const size_t LV = level_stride(ns), LC = level_copy(ns);
-                launch_pdl(mpc_prepare_kernel<Real>, std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256)), 256,
-                           qs, s > start_node, ctx.R.view, lc, state.p, s, h,
-                           cfg.use_terminal_field ? (const double*)field.p : nullptr, lad, J.p + (size_t)h * LV,
-                           J.p + (size_t)h * LV + LC);
-                ECO_CUDA(cudaGetLastError());
-                ++launches;
-                // the J-independent half of the decision runs beside the sweeps
+                const int h = horizon(s);
+                Real* Js = Jstack(s);
+                if (s == start_node) {
+                    mpc_ladders_kernel<<<1, 256, 0, qs>>>(ctx.R.view, lc, state.p, s, h, lad);
+                    mpc_seed_kernel<Real><<<seed_grid, 256, 0, qs>>>(lc, s, h, fld, Js + (size_t)h * LV,
+                                                                     Js + (size_t)h * LV + LC);
+                    ECO_CUDA(cudaGetLastError());
+                    launches += 2;
+                }
+                // beside the sweeps: the J-independent half of the decision and
+                // the next step's terminal level
                 ECO_CUDA(cudaEventRecord(dec_fork, qs));
                 ECO_CUDA(cudaStreamWaitEvent(dec_side, dec_fork, 0));
                 mpc_candidates_kernel<<<(U + kCandThreads - 1) / kCandThreads, kCandThreads, 0, dec_side>>>(
                     ctx.plant.p, ctx.R.view, lc, state.p, s, lad, dec_cand.p, dec_head.p);
-                ECO_CUDA(cudaGetLastError());
                 ++launches;
+                if (s + 1 < s_end) {
+                    const int h1 = horizon(s + 1);
+                    Real* Jn = Jstack(s + 1);
+                    mpc_seed_kernel<Real><<<seed_grid, 256, 0, dec_side>>>(lc, s + 1, h1, fld, Jn + (size_t)h1 * LV,
+                                                                          Jn + (size_t)h1 * LV + LC);
+                    ++launches;
+                }
+                ECO_CUDA(cudaGetLastError());
                 ECO_CUDA(cudaEventRecord(dec_join, dec_side));
                 for (int k = h - 1; k >= 0; --k) {
                     StageArgs<Real> a = stage_args(ctx.G, s + k, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tc);
@@ -1236,9 +1252,9 @@ struct Session : SessionBase {
                     a.dep_ok = dep.p + (size_t)k * nt;
                     a.t_dep = tdep.p + (size_t)k * nt;
                     a.wait = wait.p + (size_t)k * nt;
-                    a.J_next = J.p + (size_t)(k + 1) * LV;
+                    a.J_next = Js + (size_t)(k + 1) * LV;
                     a.J_next1 = a.J_next + LC;
-                    a.J_out = J.p + (size_t)k * LV;
+                    a.J_out = Js + (size_t)k * LV;
                     a.J_out1 = a.J_out + LC;
                     a.P_out = P.p;
                     a.status = &state.p->status;
@@ -1253,9 +1269,11 @@ struct Session : SessionBase {
                     ++stages;
                 }
                 ECO_CUDA(cudaStreamWaitEvent(qs, dec_join, 0));
+                const int s_next = s + 1 < s_end ? s + 1 : -1;
                 launch_pdl(mpc_pick_kernel<Real>, 1, std::min(kDecideThreads, (U + 31) / 32 * 32), qs, true,
-                           (const EcoPlant*)ctx.plant.p, ctx.R.view, lc, state.p, s, h, (const Real*)(J.p + LV),
-                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p, step_ns.p);
+                           (const EcoPlant*)ctx.plant.p, ctx.R.view, lc, state.p, s, h, (const Real*)(Js + LV),
+                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p, step_ns.p,
+                           s_next, s_next < 0 ? 0 : horizon(s_next));
                 ECO_CUDA(cudaGetLastError());
                 ++launches;
             }
@@ -1278,7 +1296,8 @@ struct Session : SessionBase {
             // counters of the captured loop (same structure every replay)
             stages = 0;
             for (int s = start_node; s < s_end; ++s) stages += H < n - 1 - s ? H : n - 1 - s;
-            launches = (int64_t)(s_end - start_node) * 3 + stages;   // prepare, candidates, pick + stages
+            // candidates, seed, pick per step (+ first ladders / seed) + stages
+            launches = (int64_t)(s_end - start_node) * 3 + 1 + stages;
             all.start(st);
             state.upload(&h0, 1, st);
             ECO_CUDA(cudaGraphLaunch(gexec, st));

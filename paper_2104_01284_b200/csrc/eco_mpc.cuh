@@ -1,13 +1,14 @@
 // eco_mpc.cuh — device-resident receding-horizon loop pieces.
 //
-//   prepare  <- build_context        dp.py:255-341  (ladders, terminal seed)
-//   decide   <- _argmin_at_state     mpc.py:189-278
-//              + _max_braking_decision mpc.py:490-510
-//              + propagate_state_full  plant.py:341-439
-//              + simulate_closed_loop  mpc.py:549-594 (row log, mismatch check)
+//   ladders / seed   <- build_context        dp.py:255-341  (ladders at x.t; terminal level)
+//   candidates/pick  <- _argmin_at_state     mpc.py:189-278
+//                       + _max_braking_decision mpc.py:490-510
+//                       + propagate_state_full  plant.py:341-439
+//                       + simulate_closed_loop  mpc.py:549-594 (row log, mismatch check)
 //
-// The state x = (v, soc, t) never leaves the device during a run; one
-// prepare / h stage sweeps / one decide launch per route node.
+// The state x = (v, soc, t) never leaves the device during a run.  Per route
+// node: the candidates (and the next node's terminal level) beside the h
+// stage sweeps, then one pick, which also builds the next node's ladders.
 #pragma once
 
 #include "eco_kernels.cuh"
@@ -125,39 +126,52 @@ __device__ __forceinline__ Real terminal_value(double base, double soc, double t
     return val >= j_inf ? (Real)INFINITY : (Real)val;
 }
 
-// Builds the time ladder at x.t, the node ladders of nodes s..s+h (block 0)
-// and the terminal level J_h (all blocks; grid-stride over (v, soc) cells,
-// each replicated along t, both level copies).
-template <typename Real>
-__global__ void mpc_prepare_kernel(DevRoute r, LoopCfg c, LoopState* st, int s, int h,
-                                   const double* field, Ladders lad, Real* Jh, Real* Jh1) {
-    pdl_wait();           // launched programmatically after the previous step's pick
-    if (st->status != 0) return;
-    // per-step solve clock, prepare entry -> pick entry: device timestamps
-    // instead of event nodes, which cost ~20 us per step inside the graph
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->prep_ns = globaltimer_ns();
-    const double t = st->x[2];
-    const double t0 = c.dt * floor(t / c.dt);          // GridSpec.t_axis dp.py:75-77
+// build_context (dp.py:255-341) on the device, in two x-independent /
+// x-dependent halves.
+//
+// build_ladders: the time ladder at clock t (GridSpec.t_axis dp.py:75-77),
+// the node ladders of nodes s..s+h (dp.py:217-252) and the per-stage flags;
+// one block.  Run by the pick kernel for the next step (the clock is known
+// once the decision is applied) and by mpc_ladders_kernel for a run's first
+// step.
+__device__ void build_ladders(const DevRoute& r, const LoopCfg& c, double t, int s, int h, const Ladders& lad) {
+    __shared__ double t_axis[1024];
+    const double t0 = c.dt * floor(t / c.dt);
     const int nt = c.nt;
-    if (blockIdx.x == 0) {
-        __shared__ double t_axis[1024];
-        for (int z = threadIdx.x; z < nt; z += blockDim.x) {
-            const double tz = t0 + c.dt * (double)z;
-            lad.t_axis[z] = tz;
-            if (z < 1024) t_axis[z] = tz;
-        }
-        __syncthreads();
-        const double* tax = nt <= 1024 ? t_axis : lad.t_axis;
-        for (int i = threadIdx.x; i < (h + 1) * nt; i += blockDim.x) {
-            const int k = i / nt, z = i - k * nt;
-            node_ladder(r, s + k, tax, nt, c.teleport, lad.green + k * nt, lad.dep_ok + k * nt,
-                        lad.t_dep + k * nt, lad.wait + k * nt, z);
-        }
-        if (lad.flags) {
-            __syncthreads();
-            ladder_flags(lad.green, lad.dep_ok, lad.wait, nt, h, lad.flags);
-        }
+    for (int z = threadIdx.x; z < nt; z += blockDim.x) {
+        const double tz = t0 + c.dt * (double)z;
+        lad.t_axis[z] = tz;
+        if (z < 1024) t_axis[z] = tz;
     }
+    __syncthreads();
+    const double* tax = nt <= 1024 ? t_axis : lad.t_axis;
+    for (int i = threadIdx.x; i < (h + 1) * nt; i += blockDim.x) {
+        const int k = i / nt, z = i - k * nt;
+        node_ladder(r, s + k, tax, nt, c.teleport, lad.green + k * nt, lad.dep_ok + k * nt, lad.t_dep + k * nt,
+                    lad.wait + k * nt, z);
+    }
+    if (lad.flags) {
+        __syncthreads();
+        ladder_flags(lad.green, lad.dep_ok, lad.wait, nt, h, lad.flags);
+    }
+}
+
+// The first step's ladders.  The per-step solve clock starts when a step's
+// ladders are in place (prep_ns) and stops at the pick's entry: device
+// timestamps instead of event nodes, which cost ~20 us per step in the graph.
+__global__ void mpc_ladders_kernel(DevRoute r, LoopCfg c, LoopState* st, int s, int h, Ladders lad) {
+    if (st->status != 0) return;
+    build_ladders(r, c, st->x[2], s, h, lad);
+    if (threadIdx.x == 0) st->prep_ns = globaltimer_ns();
+}
+
+// The terminal level J_h of the solve at node s (dp.py:322-334): the field
+// slice at node s + h plus the SoC penalty, replicated along t, both level
+// copies.  Independent of the vehicle state, so it runs for step s + 1 on the
+// side branch of step s (double-buffered levels).
+template <typename Real>
+__global__ void mpc_seed_kernel(LoopCfg c, int s, int h, const double* field, Real* Jh, Real* Jh1) {
+    const int nt = c.nt;
     const int ncell = c.nv * c.nx;
     const int total = ncell * nt;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -306,52 +320,12 @@ __device__ __forceinline__ bool decide_better(double f2, int u2, double f, int u
     return u2 >= 0 && (u < 0 || f2 < f || (f2 == f && u2 < u));
 }
 
-template <typename Real>
-__global__ void __launch_bounds__(kDecideThreads)
-mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
-                const Real* J1, const DecideCand* __restrict__ cand, const DecideHead* __restrict__ head,
-                Ladders lad, EcoTrajRow* rows, unsigned long long* step_ns) {
-    // launched programmatically after the last stage sweep: resident during
-    // its tail, then waits for J_1; the next step's prepare may do the same
-    pdl_launch_dependents();
-    pdl_wait();
-    if (st->status != 0) return;
-    if (threadIdx.x == 0) {                      // per-step solve clock (see mpc_prepare_kernel)
-        const unsigned long long dt = globaltimer_ns() - st->prep_ns;
-        st->sweep_ns += dt;
-        step_ns[st->n_rows] = dt;
-    }
-    const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
-    double bestf = 0.0;
-    int bestu = -1;
-    for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
-        const DecideCand* k = cand + u;
-        if (k->ok == 0.0) continue;
-        const double jn = table_interp<Real>(J1, v1, c.nv, c.soc_axis, c.nx, lad.t_axis, c.nt, c.j_inf, k->v2,
-                                             k->soc2, k->t2);
-        if (!(jn < c.j_inf)) continue;
-        const double f = k->pre + jn;
-        if (bestu < 0 || f < bestf) { bestf = f; bestu = u; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
-        const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
-        if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
-    }
-    __shared__ double s_f[kDecideThreads / 32];
-    __shared__ int s_u[kDecideThreads / 32];
-    const int nw = (int)(blockDim.x >> 5), lane = threadIdx.x & 31;
-    if (lane == 0) { s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu; }
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    bestf = lane < nw ? s_f[lane] : 0.0;
-    bestu = lane < nw ? s_u[lane] : -1;
-    for (int o = 16; o > 0; o >>= 1) {
-        const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
-        const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
-        if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
-    }
-    if (threadIdx.x != 0) return;
+// Applies the decision (thread 0): the winner's plant step, or the
+// max-brake fallback (mpc.py:490-510) and propagate_state_full; writes the
+// trajectory row and the next state, or a failure status.
+__device__ void decide_apply(const EcoPlant* __restrict__ plant, const DevRoute& r, const LoopCfg& c, LoopState* st,
+                             int s, int h, int bestu, double bestf, const DecideCand* __restrict__ cand,
+                             const DecideHead* __restrict__ head, EcoTrajRow* rows) {
     const double v = st->x[0], soc = st->x[1], t = st->x[2];
     const int src = r.kinds[s], dst = r.kinds[s + 1];
     EcoTrajRow row{};
@@ -415,6 +389,61 @@ mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopS
     rows[st->n_rows] = row;
     st->n_rows += 1;
     st->x[0] = o.v_next; st->x[1] = soc - o.dt_move * cur / P.c_nom; st->x[2] = tb_p + o.dt_move;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kDecideThreads)
+mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopState* st, int s, int h,
+                const Real* J1, const DecideCand* __restrict__ cand, const DecideHead* __restrict__ head,
+                Ladders lad, EcoTrajRow* rows, unsigned long long* step_ns, int s_next, int h_next) {
+    // launched programmatically after the last stage sweep: resident during
+    // its tail, then waits for J_1.  No early trigger: the next step's first
+    // stage reads the ladders built at the end of this kernel.
+    pdl_wait();
+    if (st->status != 0) return;
+    if (threadIdx.x == 0) {                      // per-step solve clock (see mpc_ladders_kernel)
+        const unsigned long long dt = globaltimer_ns() - st->prep_ns;
+        st->sweep_ns += dt;
+        step_ns[st->n_rows] = dt;
+    }
+    const double* v1 = c.vaxes + (size_t)(s + 1) * c.nv;
+    double bestf = 0.0;
+    int bestu = -1;
+    for (int u = threadIdx.x; u < c.U; u += blockDim.x) {
+        const DecideCand* k = cand + u;
+        if (k->ok == 0.0) continue;
+        const double jn = table_interp<Real>(J1, v1, c.nv, c.soc_axis, c.nx, lad.t_axis, c.nt, c.j_inf, k->v2,
+                                             k->soc2, k->t2);
+        if (!(jn < c.j_inf)) continue;
+        const double f = k->pre + jn;
+        if (bestu < 0 || f < bestf) { bestf = f; bestu = u; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
+        const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
+        if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
+    }
+    __shared__ double s_f[kDecideThreads / 32];
+    __shared__ int s_u[kDecideThreads / 32];
+    const int nw = (int)(blockDim.x >> 5), lane = threadIdx.x & 31;
+    if (lane == 0) { s_f[threadIdx.x >> 5] = bestf; s_u[threadIdx.x >> 5] = bestu; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        bestf = lane < nw ? s_f[lane] : 0.0;
+        bestu = lane < nw ? s_u[lane] : -1;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double f2 = __shfl_down_sync(0xffffffffu, bestf, o);
+            const int u2 = __shfl_down_sync(0xffffffffu, bestu, o);
+            if (decide_better(f2, u2, bestf, bestu)) { bestf = f2; bestu = u2; }
+        }
+        if (threadIdx.x == 0) decide_apply(plant, r, c, st, s, h, bestu, bestf, cand, head, rows);
+    }
+    if (s_next < 0) return;
+    // the next step's ladders at the new clock (build_context's x-dependent half)
+    __syncthreads();
+    if (st->status != 0) return;
+    build_ladders(r, c, st->x[2], s_next, h_next, lad);
+    if (threadIdx.x == 0) st->prep_ns = globaltimer_ns();
 }
 
 // Batch scenarios (C4): per scenario b the time ladder at t_start[b]
