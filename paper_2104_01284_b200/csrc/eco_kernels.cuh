@@ -722,9 +722,18 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     // wait, no stop dwell, departures always allowed) moves exactly like a
     // moving one (K:528-533).  Precomputed per stage (flags) when available.
     bool any_red, any_hold;
-    // (the wide-row kernel keeps the in-kernel scan: measured 20 % faster
-    // there, its prologue being a negligible part of a 45,500-CTA launch)
-    if (!WIDE && a.flags) {
+    // Single solves: moving planes take the flags (and the arrival mask)
+    // after the grid dependency wait -- an MPC step's first stage starts while
+    // the previous pick still builds them.  (The batch kernel keeps the early
+    // read; the wide-row kernel keeps the in-kernel scan: measured 20 % faster
+    // there, its prologue being a negligible part of a 45,500-CTA launch.)
+    bool late = false;
+    if constexpr (!WIDE && PREFETCH) late = a.flags && v > 0.0;
+    if (late) {
+        any_red = false;               // set after pdl_wait below
+        any_hold = false;              // a moving plane never holds
+    } else if (!WIDE && a.flags) {
+        if constexpr (PREFETCH) pdl_wait();   // the flags may come from the previous kernel
         const int fl = *a.flags;
         any_red = (fl & kStageAnyRed) != 0;
         any_hold = (fl & kStageAnyHold) != 0 && v == 0.0;
@@ -758,6 +767,15 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
     RowRec2<Real>* s_rr = (RowRec2<Real>*)(smem + L.rr);
     ActRec<Real>* s_act = (ActRec<Real>*)(smem + L.act);
     const bool staged = !WIDE && fast && nseg >= 0 && count <= a.count_max;
+    if constexpr (!WIDE && PREFETCH) {
+        if (late && !staged) {        // (rare) unstaged moving tile
+            pdl_wait();
+            any_red = (*a.flags & kStageAnyRed) != 0;
+            if (any_red)
+                for (int i = threadIdx.x; i < nt; i += blockDim.x) s_green[i] = a.green[i];
+            __syncthreads();
+        }
+    }
     if (staged) {
         // ---- stage with cp.async: the plane's action records and the tile's
         //      row records (route geometry), then -- once the previous stage
@@ -787,6 +805,13 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                     if (sizeof(Real) == 4) cp_async4(dst + i, src + i);
                     else dst[i] = src[i];
                 }
+            }
+        }
+        if constexpr (!WIDE && PREFETCH) {
+            if (late) {               // while the band copies are in flight
+                any_red = (*a.flags & kStageAnyRed) != 0;
+                if (any_red)
+                    for (int i = threadIdx.x; i < nt; i += blockDim.x) s_green[i] = a.green[i];
             }
         }
         cp_async_wait_all();

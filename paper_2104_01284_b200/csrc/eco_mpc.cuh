@@ -397,8 +397,10 @@ mpc_pick_kernel(const EcoPlant* __restrict__ plant, DevRoute r, LoopCfg c, LoopS
                 const Real* J1, const DecideCand* __restrict__ cand, const DecideHead* __restrict__ head,
                 Ladders lad, EcoTrajRow* rows, unsigned long long* step_ns, int s_next, int h_next) {
     // launched programmatically after the last stage sweep: resident during
-    // its tail, then waits for J_1.  No early trigger: the next step's first
-    // stage reads the ladders built at the end of this kernel.
+    // its tail, then waits for J_1.  The next step's first stage may start
+    // its prologue early: it reads the ladders built at the end of this
+    // kernel only after its own grid dependency wait.
+    pdl_launch_dependents();
     pdl_wait();
     if (st->status != 0) return;
     if (threadIdx.x == 0) {                      // per-step solve clock (see mpc_ladders_kernel)
