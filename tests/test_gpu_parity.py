@@ -522,3 +522,33 @@ def test_closed_loop_step_clocks(vehicle, short_route):
     assert abs(w.sum() * 1e3 - traj.stats["dominant_ms"]) <= 1e-6 * max(1.0, traj.stats["dominant_ms"])
     dec = mpc.control(StateVector(v=5.0, soc=0.5, t=0.0), 3)
     assert 0 < dec.solver_wall_s < 0.05
+
+
+DIFF = GridSpec(n_v=20, n_soc=14, n_t=40, n_t_eng=16, n_t_bsg=20)
+
+
+@pytest.mark.parametrize("kind,seed,grid,horizon,gamma,teleport", [
+    ("short", 2, SMALL, 8, 0.0, True),        # max-brake fallbacks on the way
+    ("short", 2, SMALL, 8, 1.0, False),       # red light without teleport: the plant step fails at node 54
+    ("mixed", 1, DIFF, 20, 0.5, True),
+    ("mixed", 1, DIFF, 20, 0.25, False),
+    ("urban", 3, DIFF, 20, 0.8, True),
+])
+def test_closed_loop_variants_fp64_vs_oracle(vehicle, kind, seed, grid, horizon, gamma, teleport):
+    """Whole closed loops (field, every solve, decision, plant step) on other
+    routes, trade-offs and teleport settings: rows, status, failure node and
+    final state bit for bit against the oracle's closed loop."""
+    from paper_2104_01284_b200 import load_fixture_route
+    route, spat = load_fixture_route(kind, seed=seed)
+    fld = O.field_build(vehicle, route, spat, grid, PEN, gamma)
+    ref = O.mpc_run(vehicle, route, spat, grid, PEN, gamma, horizon, (0.0, 0.5, 0.0), fld, teleport=teleport)
+    mpc = EcoDrivingMPC(vehicle, gamma=gamma, grids=grid, penalty=PEN, horizon=horizon, backend="b200-fp64",
+                        teleport=teleport).fit(route, spat)
+    assert np.array_equal(mpc.terminal_field_.values, fld)
+    rows, status, node, fin, _ = mpc.session_.run(StateVector(v=0.0, soc=0.5, t=0.0))
+    assert (status, len(rows)) == (ref["status"], len(ref["rows"]))
+    if status != 0:
+        assert node == ref["status_node"]
+    for f in rows.dtype.names:
+        assert np.array_equal(rows[f], ref["rows"][f], equal_nan=True), f
+    assert np.array_equal(fin, ref["final"])
