@@ -552,3 +552,19 @@ def test_closed_loop_variants_fp64_vs_oracle(vehicle, kind, seed, grid, horizon,
     for f in rows.dtype.names:
         assert np.array_equal(rows[f], ref["rows"][f], equal_nan=True), f
     assert np.array_equal(fin, ref["final"])
+
+
+@pytest.mark.parametrize("kind,seed,gamma", [("mixed", 1, 0.5), ("urban", 3, 0.8)])
+def test_closed_loop_variants_fp32_within_0p1pct(vehicle, kind, seed, gamma):
+    """fp32 production loop on other routes: fuel and travel time within 0.1 %
+    of the oracle's fp64 closed loop (north_star's closed-loop bar)."""
+    from paper_2104_01284_b200 import load_fixture_route
+    route, spat = load_fixture_route(kind, seed=seed)
+    fld = O.field_build(vehicle, route, spat, DIFF, PEN, gamma)
+    ref = O.mpc_run(vehicle, route, spat, DIFF, PEN, gamma, 20, (0.0, 0.5, 0.0), fld)
+    mpc = EcoDrivingMPC(vehicle, gamma=gamma, grids=DIFF, penalty=PEN, horizon=20, backend="b200").fit(route, spat)
+    traj = simulate_closed_loop(route, spat, mpc)
+    assert traj.status == "ok" and ref["status"] == 0
+    fuel_ref = float(np.sum(ref["rows"]["fuel_inc_g"]))
+    assert abs(traj.fuel_g - fuel_ref) <= 1e-3 * fuel_ref, (traj.fuel_g, fuel_ref)
+    assert abs(traj.final_state.t - ref["final"][2]) <= 1e-3 * ref["final"][2], (traj.final_state.t, ref["final"][2])
