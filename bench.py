@@ -267,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic": f"{FLOPS_PER_LIVE} flop x {live} live gathers per step / summed sweep time"},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:      # the CPU sample runs at N = 1 only
         out["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     if dist is not None:
         dist.destroy_process_group()
@@ -459,7 +459,7 @@ def run_c4(args, rank, world, local_rank):
         "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_batch_kernel"),
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = c4_cpu_baseline(args.cpu_seconds)
     if dist is not None:
         dist.destroy_process_group()
@@ -549,7 +549,7 @@ def run_c3(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     del res
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         from oracle import oracle as O
         c = c3_context(H=1)
         t0 = time.perf_counter()
