@@ -847,10 +847,15 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 } else {
                     ro = rows2[k * tjs];
                 }
-                if (z0 > ro.zlim) continue;                      // also: SoC move off the hull
+                // single solves take no branch here (C2 -1.1 %): a thread past
+                // the row's last live state (also: SoC move off the hull) reads
+                // the row's first samples, inside the band, and its masks
+                // reject them
+                const int zq = (PREFETCH && z0 > ro.zlim) ? 0 : z0;
+                if (!PREFETCH && z0 > ro.zlim) continue;
                 if (!PREFETCH) rc = s_act[k];
-                const Real* plo = s_band + ro.blo + z0;          // (ivlo, jxlo, t' = z0 + zoff)
-                const Real* phi = s_band + ro.bhi + z0;          // (ivhi, jxlo, t')
+                const Real* plo = s_band + ro.blo + zq;          // (ivlo, jxlo, t' = z0 + zoff)
+                const Real* phi = s_band + ro.bhi + zq;          // (ivhi, jxlo, t')
                 const int dx = ro.wx > (Real)0 ? nt : 0;
                 // fp32: one weighted corner sum per t pair with the stage
                 // cost folded in (it cancels in the time blend): 4 FFMA2
