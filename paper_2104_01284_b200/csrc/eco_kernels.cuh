@@ -836,14 +836,28 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
             // gain from it (C4 +5 %)
             RowRec2<Real> ro_n{};
             ActRec<Real> rc_n{};
-            if (PREFETCH && slice < count) { ro_n = rows2[slice * tjs]; rc_n = s_act[slice]; }
+            // (shared-memory byte addresses of the next records, advanced by
+            // constant strides: no per-iteration index products)
+            const unsigned ro_step = (unsigned)(slices * tjs * (int)sizeof(RowRec2<Real>));
+            const unsigned rc_step = (unsigned)(slices * (int)sizeof(ActRec<Real>));
+            const char* ro_p = reinterpret_cast<const char*>(rows2 + slice * tjs);
+            const char* rc_p = reinterpret_cast<const char*>(s_act + slice);
+            if (PREFETCH && slice < count) {
+                ro_n = *reinterpret_cast<const RowRec2<Real>*>(ro_p);
+                rc_n = *reinterpret_cast<const ActRec<Real>*>(rc_p);
+            }
             for (int k = slice; k < count; k += slices) {
                 RowRec2<Real> ro;
                 ActRec<Real> rc;
                 if (PREFETCH) {
                     ro = ro_n;
                     rc = rc_n;
-                    if (k + slices < count) { ro_n = rows2[(k + slices) * tjs]; rc_n = s_act[k + slices]; }
+                    ro_p += ro_step;
+                    rc_p += rc_step;
+                    if (k + slices < count) {
+                        ro_n = *reinterpret_cast<const RowRec2<Real>*>(ro_p);
+                        rc_n = *reinterpret_cast<const ActRec<Real>*>(rc_p);
+                    }
                 } else {
                     ro = rows2[k * tjs];
                 }
