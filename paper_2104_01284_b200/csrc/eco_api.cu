@@ -1088,7 +1088,6 @@ struct Session : SessionBase {
     DBuf<double> tdep, wait, tax;
     DBuf<int> sflags;              // kStageAny* per stage of the current solve
     DBuf<Real> J;
-    DBuf<int32_t> P;
     DBuf<EcoTrajRow> rows;
     DBuf<unsigned long long> live;
     cudaStream_t st = 0;
@@ -1117,7 +1116,6 @@ struct Session : SessionBase {
         tdep.alloc((size_t)(H + 1) * nt); wait.alloc((size_t)(H + 1) * nt); tax.alloc(nt);
         sflags.alloc(H);
         J.alloc((size_t)2 * (H + 1) * level_stride(ns));   // two stacks, alternating by step
-        P.alloc(ns);
         rows.alloc(n - 1);
         live.alloc(1);
         ECO_CUDA(cudaStreamSynchronize(st));
@@ -1256,7 +1254,9 @@ struct Session : SessionBase {
                     a.J_next1 = a.J_next + LC;
                     a.J_out = Js + (size_t)k * LV;
                     a.J_out1 = a.J_out + LC;
-                    a.P_out = P.p;
+                    // the closed loop decides at the exact state from J_1
+                    // (mpc.py:189-278): no policy table is needed
+                    a.P_out = nullptr;
                     a.status = &state.p->status;
                     a.live = count ? live.p : nullptr;
                     a.src_kind = kinds[s + k];
