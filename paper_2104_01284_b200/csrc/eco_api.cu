@@ -260,7 +260,8 @@ struct Geometry {
     DBuf<RowRec2<Real>> row2;
     DBuf<TilePlan> tiles;
     DBuf<int32_t> order, rank_of;
-    int h_gmax[4] = {0, 0, 0, 0};     // max feasible actions of a plane
+    int h_gmax[4] = {0, 0, 0, 0};     // [0] max feasible actions of a plane, [1] some tile unstaged
+    bool all_staged = false;          // every tile stages its band: no kernel reads the shifted copy
     int64_t rows_total = 0;
     int tj = 0, nchunk = 0, band_cap = 0;   // stage-kernel tile shape the plans were built for
     int plo = 0, phi = -1;                  // tiles of planes [plo, phi) ordered first (slab solves)
@@ -341,6 +342,9 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
             G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
     }
     ECO_CUDA(cudaGetLastError());
+    ECO_CUDA(cudaMemcpyAsync(&G.h_gmax[1], G.gmax.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ECO_CUDA(cudaStreamSynchronize(st));
+    G.all_staged = G.h_gmax[1] == 0 && !wide_rows(g.nt);
     if (launches) *launches += 6;
 }
 
@@ -1253,7 +1257,8 @@ struct Session : SessionBase {
                     a.J_next = Js + (size_t)(k + 1) * LV;
                     a.J_next1 = a.J_next + LC;
                     a.J_out = Js + (size_t)k * LV;
-                    a.J_out1 = a.J_out + LC;
+                    // the shifted copy only serves unstaged tiles (global-memory pair loads)
+                    a.J_out1 = ctx.G.all_staged ? nullptr : a.J_out + LC;
                     // the closed loop decides at the exact state from J_1
                     // (mpc.py:189-278): no policy table is needed
                     a.P_out = nullptr;
@@ -1282,7 +1287,8 @@ struct Session : SessionBase {
         if (use_graph) {
             const std::vector<long long> key = {start_node, s_end, (long long)(size_t)ctx.G.row2.p,
                                                 (long long)(size_t)ctx.G.tiles.p, (long long)(size_t)ctx.G.order.p,
-                                                (long long)(size_t)field.p, tc.tj, tc.slices};
+                                                (long long)(size_t)field.p, tc.tj, tc.slices,
+                                                ctx.G.all_staged ? 1 : 0};
             if (!gexec || key != gkey) {
                 if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
                 cudaGraph_t graph;

@@ -327,6 +327,7 @@ geom_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int band_cap
         tp->nseg = ok ? ns : -1;
         tp->band = ok ? run : 0;
         s_ok = ok;
+        if (!ok) atomicOr(&g.gmax[1], 1);
         (void)s_base;
     }
     __syncthreads();
@@ -420,6 +421,7 @@ geom_plane_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int ba
         tp->nseg = ok ? ns : -1;
         tp->band = ok ? run : 0;
         s_ok[c] = ok;
+        if (!ok) atomicOr(&g.gmax[1], 1);            // some tile reads J_next outside the band
     }
     __syncthreads();
     RowRec2<Real>* out = row2 + roff;
@@ -706,7 +708,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         pdl_wait();
         for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
             a.J_out[obase + f] = (Real)INFINITY;
-            if (obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
+            if (a.J_out1 && obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
             if (a.P_out) a.P_out[obase + f] = -1;
             if (PEERS) store_peers(a, obase + f, (Real)INFINITY);
         }
@@ -1281,7 +1283,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         if (!live) continue;
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
-        if (obase + f > 0) a.J_out1[obase + f - 1] = val;
+        if (a.J_out1 && obase + f > 0) a.J_out1[obase + f - 1] = val;
         if (PEERS) store_peers(a, obase + f, val);
         if (a.P_out) a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
     }
