@@ -247,7 +247,8 @@ int32_t eco_session_create(const EcoPlant* plant, const EcoRoute* route,
                            const EcoMpcConfig* cfg, EcoSession** out);
 /* new data for the session's route (same node count): speed limits,
  * grades, node kinds, signal programs; the next fit rebuilds geometry and
- * field from it. */
+ * field from it (EcoDrivingMPC.fit(route, spat) mpc.py:379-391 on a new
+ * route / SPaT of the same shape). */
 int32_t eco_session_upload_route(EcoSession* sess, const EcoRoute* route);
 int32_t eco_session_fit(EcoSession* sess, const double* field_in,
                         double* field_out, EcoStats* stats);
@@ -255,9 +256,10 @@ int32_t eco_session_run(EcoSession* sess, int32_t start_node, int32_t max_steps,
                         const double* x_start, EcoTrajRow* rows, int32_t* n_rows,
                         int32_t* status, int32_t* status_node,
                         double* final_state, int32_t flags, EcoStats* stats);
-/* per-step solve clocks (ms, device timestamps: context preparation entry ->
- * decision entry) of the last eco_session_run's first n steps (n <= the
- * steps that run took). */
+/* per-step solve clocks (ms, device timestamps: context in place -> decision
+ * entry) of the last eco_session_run's first n steps (n <= the steps that
+ * run took): ClosedLoopTrajectory.solver_wall_s (mpc.py:438-487), written by
+ * write_timing_csv (io.py:115-124). */
 int32_t eco_session_step_times(EcoSession* sess, double* solve_ms, int32_t n);
 int32_t eco_session_destroy(EcoSession* sess);
 
