@@ -40,6 +40,17 @@ class TerminalCostField:
     def node_slice(self, s: int) -> np.ndarray:
         return self.values[s]
 
+    @classmethod
+    def _from_device(cls, values: np.ndarray, **kw) -> "TerminalCostField":
+        """A field the device just built (shape known, NaN impossible by
+        construction: +inf / j_inf only): skips the user-input checks of
+        __post_init__ (a 5 MB NaN scan per fit at C2)."""
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "values", values)
+        for k, v in kw.items():
+            object.__setattr__(obj, k, v)
+        return obj
+
     def __post_init__(self):
         if self.values.ndim != 3:
             raise ValueError("terminal field values must be (nodes, n_v, n_soc)")
@@ -396,7 +407,7 @@ class EcoDrivingMPC:
         # been edited in place since): ~150 KB per fit, the inputs' H2D
         self.upload_bytes_ = self.session_.upload_route(route, spat)
         values, self.fit_stats_ = self.session_.fit()
-        self.terminal_field_ = (TerminalCostField(values=values, route_name=route.name, gamma=self.gamma,
+        self.terminal_field_ = (TerminalCostField._from_device(values, route_name=route.name, gamma=self.gamma,
                                                   grids=self.grids, penalty=self.penalty)
                                 if self.use_terminal_field else None)
         return self
