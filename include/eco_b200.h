@@ -54,6 +54,12 @@ extern "C" {
 /* precision selector */
 #define ECO_FP32 0
 #define ECO_FP64 1
+/* OR-ed into the precision argument of eco_bellman_step / eco_solve_horizon /
+ * eco_solve_tables: ties go to the HIGHEST flat action index instead of the
+ * lowest (perturb_ties / reverse_ties, dp.py:365-404, _kernels.py:630-632 and
+ * 738-740: the negative control of the backend-diff harness; costs are
+ * unchanged, tied policy entries flip). */
+#define ECO_REVERSE_TIES 0x100
 
 /* node kinds (route.py:29-31) */
 #define ECO_NODE_PLAIN 0

@@ -27,6 +27,7 @@ SLAB_INFO_BYTES = 256
 
 OK, ERR_ARG, ERR_CUDA, ERR_NODEV = 0, 1, 2, 3
 FP32, FP64 = 0, 1
+REVERSE_TIES = 0x100          # OR-ed into the precision argument (perturb_ties)
 RUN_OK, RUN_INFEASIBLE, RUN_PLANT, RUN_MISMATCH = 0, 1, 2, 3
 RUN_COUNT_LIVE, RUN_TIME_SWEEPS = 1, 2
 

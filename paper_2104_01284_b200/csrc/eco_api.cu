@@ -323,8 +323,10 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
     if (G.order.n != ntiles) { G.order.alloc(ntiles); G.rank_of.alloc(ntiles); }
     const int phi = G.phi < 0 ? g.nv : G.phi;
-    const int light = light_first<Real>(G, g.nt, (phi - G.plo) * G.nchunk);
-    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, phi, light, G.order.p, G.rank_of.p);
+    const int chunk_major = env_int("ECO_CHUNK_MAJOR", wide_rows(g.nt) ? 1 : 0);
+    const int light = chunk_major ? 0 : light_first<Real>(G, g.nt, (phi - G.plo) * G.nchunk);
+    geom_order_kernel<<<g.P, 256, 0, st>>>(G.count.p, g.nv, G.nchunk, G.plo, phi, light, chunk_major, G.order.p,
+                                           G.rank_of.p);
     ECO_CUDA(cudaGetLastError());
     // one block per (plan, plane) covering all its SoC chunks (coalesced row
     // records); the per-tile kernel remains for grids whose chunk tables
@@ -476,13 +478,17 @@ int light_first(const Geometry<Real>& G, int nt, int nlaunch) {
 }
 
 template <typename Real, int MODE>
-void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st, int ntiles = -1) {
+void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaStream_t st, int ntiles = -1,
+                  bool rev = false) {
     const unsigned grid = (unsigned)(ntiles >= 0 ? ntiles : a.nv * tc.nchunk);
     const unsigned block = (unsigned)(tc.S * tc.slices);
     if (MODE == 0) {
         using KT = void (*)(StageArgs<Real>);
         KT k;
-        if (a.npeer > 0)
+        if (rev) {   // perturb_ties (highest index wins ties): plain solves only
+            if (count || a.npeer > 0) throw ArgError{"perturb_ties: not with live counting or slab exchange"};
+            k = tc.wide ? bellman_wide_kernel<Real, false, false, true> : bellman_stage_kernel<Real, false, false, true>;
+        } else if (a.npeer > 0)
             k = tc.wide ? (count ? bellman_wide_kernel<Real, true, true> : bellman_wide_kernel<Real, false, true>)
                         : (count ? bellman_stage_kernel<Real, true, true> : bellman_stage_kernel<Real, false, true>);
         else
@@ -654,6 +660,14 @@ struct HorizonInputs {
     }
 };
 
+// The stateless solvers share one workspace (inputs block, tables, geometry,
+// the overlap stream): calls from several host threads are serialised here
+// (ctypes releases the GIL, so Python threads do reach this concurrently).
+inline std::mutex& workspace_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
 inline HorizonInputs& horizon_inputs() {
     static HorizonInputs in;
     return in;
@@ -683,9 +697,10 @@ HorizonWorkspace<Real>& horizon_workspace() {
 template <typename Real>
 void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H,
                         const EcoStage1Tables* tabs, const double* terminal, double* J_stack, int32_t* P_stack,
-                        bool count, EcoStats* stats) {
+                        bool count, EcoStats* stats, bool rev = false) {
     const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t, U = pr->n_te * pr->n_tb;
     const size_t ns = (size_t)nv * nx * nt;
+    std::lock_guard<std::mutex> lock(workspace_mutex());
     cudaStream_t st = 0;
     int64_t launches = 0;
     HorizonInputs& in = horizon_inputs();
@@ -773,7 +788,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             ECO_CUDA(cudaMemsetAsync(dbgbuf.p, 0, dbgbuf.n * 8, st));
             a.dbg = dbgbuf.p;
         }
-        launch_stage<Real, 0>(a, tc, count, st);
+        launch_stage<Real, 0>(a, tc, count, st, -1, rev);
         if (overlap) ECO_CUDA(cudaEventRecord(lvl_ev[k], st));
         if (dbg_on) {
             std::vector<unsigned long long> h(dbgbuf.n);
@@ -1146,11 +1161,15 @@ struct Session : SessionBase {
     void upload_route(const EcoRoute* r) override {
         if (r->node_count != n) throw ArgError{"route node count differs from the session's"};
         if (!r->kinds) throw ArgError{"null route array"};
-        const bool same_kinds = std::equal(kinds.begin(), kinds.end(), r->kinds) && stop_dwell == r->stop_dwell;
+        // node kinds, dwell, spacing and comfort box are kernel arguments
+        // baked into the captured graphs (ctx.R.view is passed by value)
+        const bool same_kinds = std::equal(kinds.begin(), kinds.end(), r->kinds) && stop_dwell == r->stop_dwell &&
+                                r->delta_d == ctx.R.view.delta_d && r->accel_min == ctx.R.view.accel_min &&
+                                r->accel_max == ctx.R.view.accel_max;
         ctx.reupload(r, &cfg, st);
         kinds.assign(r->kinds, r->kinds + n);
         stop_dwell = r->stop_dwell;
-        if (!same_kinds) {           // node kinds / dwell are baked into the captured graphs
+        if (!same_kinds) {
             if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
             gkey.clear();
             if (fgraph.exec) { cudaGraphExecDestroy(fgraph.exec); fgraph.exec = nullptr; }
@@ -1837,6 +1856,7 @@ const char* eco_last_error(void) { return g_err.c_str(); }
 
 int32_t eco_release_workspace(void) {
     return run_guarded([&] {
+        std::lock_guard<std::mutex> lock(workspace_mutex());
         horizon_workspace<float>().release();
         horizon_workspace<double>().release();
     });
@@ -1856,11 +1876,15 @@ int32_t eco_bellman_step(const EcoPlant* plant, const EcoProblem* prob, const Ec
         check_problem(prob);
         if (!plan || !J_next || !J_out || !P_out) throw ArgError{"null pointer argument"};
         const size_t ns = (size_t)prob->n_v * prob->n_soc * prob->n_t;
+        const bool rev = (precision & ECO_REVERSE_TIES) != 0;
+        precision &= ~ECO_REVERSE_TIES;
         std::vector<double> stack(2 * ns);
         if (precision == ECO_FP64)
-            solve_horizon_impl<double>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats);
+            solve_horizon_impl<double>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats,
+                                       rev);
         else
-            solve_horizon_impl<float>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats);
+            solve_horizon_impl<float>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats,
+                                      rev);
         std::memcpy(J_out, stack.data(), ns * sizeof(double));
     });
 }
@@ -1873,10 +1897,14 @@ int32_t eco_solve_horizon(const EcoPlant* plant, const EcoProblem* prob, const E
         check_problem(prob);
         if (H < 1) throw ArgError{"horizon must be >= 1"};
         if (!plans || !terminal || !J_stack || !P_stack) throw ArgError{"null pointer argument"};
+        const bool rev = (precision & ECO_REVERSE_TIES) != 0;
+        precision &= ~ECO_REVERSE_TIES;
         if (precision == ECO_FP64)
-            solve_horizon_impl<double>(plant, prob, plans, H, nullptr, terminal, J_stack, P_stack, count_live, stats);
+            solve_horizon_impl<double>(plant, prob, plans, H, nullptr, terminal, J_stack, P_stack, count_live, stats,
+                                       rev);
         else
-            solve_horizon_impl<float>(plant, prob, plans, H, nullptr, terminal, J_stack, P_stack, count_live, stats);
+            solve_horizon_impl<float>(plant, prob, plans, H, nullptr, terminal, J_stack, P_stack, count_live, stats,
+                                      rev);
     });
 }
 
@@ -1887,10 +1915,12 @@ int32_t eco_solve_tables(const EcoPlant* plant, const EcoProblem* prob, const Ec
         check_plant(plant);
         check_problem(prob);
         if (H < 1 || !plans || !tables || !terminal || !J_stack || !P_stack) throw ArgError{"bad arguments"};
+        const bool rev = (precision & ECO_REVERSE_TIES) != 0;
+        precision &= ~ECO_REVERSE_TIES;
         if (precision == ECO_FP64)
-            solve_horizon_impl<double>(plant, prob, plans, H, tables, terminal, J_stack, P_stack, false, nullptr);
+            solve_horizon_impl<double>(plant, prob, plans, H, tables, terminal, J_stack, P_stack, false, nullptr, rev);
         else
-            solve_horizon_impl<float>(plant, prob, plans, H, tables, terminal, J_stack, P_stack, false, nullptr);
+            solve_horizon_impl<float>(plant, prob, plans, H, tables, terminal, J_stack, P_stack, false, nullptr, rev);
     });
 }
 

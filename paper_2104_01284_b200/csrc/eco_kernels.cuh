@@ -456,8 +456,13 @@ geom_plane_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int ba
 // CTAs): the `light` lightest launched tiles go first -- they finish early and
 // free their slots for the tail of the heavy ones, instead of forming a
 // second wave behind the heaviest tiles.
+// chunk_major (wide-row grids): the launch sweeps SoC chunk by SoC chunk
+// across all planes instead, so the CTAs resident at any moment gather from a
+// narrow SoC window of J_{k+1} (every destination plane, a few rows): that
+// window stays L2-resident while the whole level does not.
 __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int nchunk, int plo, int phi,
-                                  int light, int32_t* __restrict__ order, int32_t* __restrict__ rank_of) {
+                                  int light, int chunk_major, int32_t* __restrict__ order,
+                                  int32_t* __restrict__ rank_of) {
     const int p = blockIdx.x;
     const int32_t* c = count + (size_t)p * nv;
     const size_t base = (size_t)p * nv * nchunk;
@@ -471,9 +476,12 @@ __global__ void geom_order_kernel(const int32_t* __restrict__ count, int nv, int
             const bool jin = j >= plo && j < phi;
             r += (jin && !in) || (jin == in && ((wj > w) || (wj == w && j < iv)));
         }
+        const int np_in = phi - plo;
         for (int ch = 0; ch < nchunk; ++ch) {
             int rank = r * nchunk + ch;
-            if (light > 0 && rank < nlaunch)
+            if (chunk_major)
+                rank = in ? ch * np_in + r : np_in * nchunk + ch * (nv - np_in) + (r - np_in);
+            else if (light > 0 && rank < nlaunch)
                 rank = rank >= nlaunch - light ? rank - (nlaunch - light) : rank + light;
             order[base + rank] = iv * nchunk + ch;
             rank_of[base + iv * nchunk + ch] = rank;
@@ -688,7 +696,17 @@ __device__ __forceinline__ void store_peers(const StageArgs<Real>& a, size_t i, 
     }
 }
 
-template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false, bool PREFETCH = false>
+// Candidate acceptance of one thread's action scan (ascending flat index):
+// strict < keeps the first (lowest-index) minimiser, the reference's rule
+// (K:542-545, K:738-740); REV (perturb_ties, K:630-632) takes <= so the last
+// (highest-index) minimiser wins instead.
+template <bool REV, typename Real>
+__device__ __forceinline__ bool improves(Real F, Real best) {
+    if constexpr (REV) return F <= best;
+    else return F < best;
+}
+
+template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false, bool PREFETCH = false, bool REV = false>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
@@ -918,14 +936,14 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                     for (int i = 0; i < kZP; ++i) {
                         const bool ok = z0 + i <= ro.zlim && s_green[tz0 + i] != 0;   // K:516
                         if (COUNT) nlive += ok;
-                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                        if (ok && improves<REV>(F[i], best[i])) { best[i] = F[i]; bk[i] = k; }
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < kZP; ++i) {
                         const bool ok = z0 + i <= ro.zlim;
                         if (COUNT) nlive += ok;
-                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                        if (ok && improves<REV>(F[i], best[i])) { best[i] = F[i]; bk[i] = k; }
                     }
                 }
             }
@@ -1059,8 +1077,8 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                         const bool ok0 = z <= zl && s_green[z + zoff] != 0;       // K:516
                         const bool ok1 = z + 1 <= zl && s_green[z + 1 + zoff] != 0;
                         if (COUNT) nlive += ok0 + ok1;
-                        const bool u0 = ok0 && F[m].x < best[2 * m];
-                        const bool u1 = ok1 && F[m].y < best[2 * m + 1];
+                        const bool u0 = ok0 && improves<REV>(F[m].x, best[2 * m]);
+                        const bool u1 = ok1 && improves<REV>(F[m].y, best[2 * m + 1]);
                         best[2 * m] = u0 ? F[m].x : best[2 * m];
                         bk[2 * m] = u0 ? k : bk[2 * m];
                         best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
@@ -1071,8 +1089,8 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
 #pragma unroll
                     for (int m = 0; m < kMW; ++m) {
                         if (COUNT) nlive += 2;
-                        const bool u0 = F[m].x < best[2 * m];
-                        const bool u1 = F[m].y < best[2 * m + 1];
+                        const bool u0 = improves<REV>(F[m].x, best[2 * m]);
+                        const bool u1 = improves<REV>(F[m].y, best[2 * m + 1]);
                         best[2 * m] = u0 ? F[m].x : best[2 * m];
                         bk[2 * m] = u0 ? k : bk[2 * m];
                         best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
@@ -1084,8 +1102,8 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                         const int z = zb + 64 * m;
                         const bool ok0 = z <= zl, ok1 = z < zl;
                         if (COUNT) nlive += ok0 + ok1;
-                        const bool u0 = (F[m].x < best[2 * m]) & ok0;
-                        const bool u1 = (F[m].y < best[2 * m + 1]) & ok1;
+                        const bool u0 = improves<REV>(F[m].x, best[2 * m]) & ok0;
+                        const bool u1 = improves<REV>(F[m].y, best[2 * m + 1]) & ok1;
                         best[2 * m] = u0 ? F[m].x : best[2 * m];
                         bk[2 * m] = u0 ? k : bk[2 * m];
                         best[2 * m + 1] = u1 ? F[m].y : best[2 * m + 1];
@@ -1166,7 +1184,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                     if (COUNT) nlive += kZP;
 #pragma unroll
                     for (int i = 0; i < kZP; ++i)
-                        if (F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                        if (improves<REV>(F[i], best[i])) { best[i] = F[i]; bk[i] = k; }
                 } else {
                     const bool gate = any_red && (rc.meta & kRecGated);
                     const int tz0 = z0 + (int)(rc.meta & kRecZoff);  // arrival sample of state z0
@@ -1175,7 +1193,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                         bool ok = z0 + i <= ro.zlim;
                         if (gate && ok) ok = s_green[tz0 + i] != 0;  // K:516
                         if (COUNT) nlive += ok;
-                        if (ok && F[i] < best[i]) { best[i] = F[i]; bk[i] = k; }
+                        if (ok && improves<REV>(F[i], best[i])) { best[i] = F[i]; bk[i] = k; }
                     }
                 }
             }
@@ -1234,7 +1252,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 Real F;
                 if (reloc) F = (Real)(a.c1d[(size_t)iv * a.U + k] + (1.0 - a.gamma) * hold) + jn;   // K:542
                 else F = rc.c1 + jn;
-                if (F < best) { best = F; bk = k; }
+                if (improves<REV>(F, best)) { best = F; bk = k; }
             }
             s_best[slice * tj_nt + f] = best;
             s_arg[slice * tj_nt + f] = bk;
@@ -1271,13 +1289,13 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 const int k2 = s_arg[s * tj_nt + f];
                 if (k2 < 0) continue;
                 const Real b2 = s_best[s * tj_nt + f];
-                if (bk < 0 || b2 < best || (b2 == best && k2 < bk)) { best = b2; bk = k2; }
+                if (bk < 0 || b2 < best || (b2 == best && (REV ? k2 > bk : k2 < bk))) { best = b2; bk = k2; }
             }
         }
         if (pair) {
             const Real b2 = __shfl_xor_sync(0xffffffffu, best, 1);
             const int k2 = __shfl_xor_sync(0xffffffffu, bk, 1);
-            if (k2 >= 0 && (bk < 0 || b2 < best || (b2 == best && k2 < bk))) { best = b2; bk = k2; }
+            if (k2 >= 0 && (bk < 0 || b2 < best || (b2 == best && (REV ? k2 > bk : k2 < bk)))) { best = b2; bk = k2; }
             if (half) continue;
         }
         if (!live) continue;
@@ -1298,25 +1316,25 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
 #ifndef ECO_STAGE_MINB
 #define ECO_STAGE_MINB 3
 #endif
-template <typename Real, bool COUNT, bool PEERS = false>
+template <typename Real, bool COUNT, bool PEERS = false, bool REV = false>
 __global__ void __launch_bounds__(256, ECO_STAGE_MINB)
 bellman_stage_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     // (a stopped closed loop (a.status) needs no early exit here: prepare and
     // decide skip, so this stage's output is never read)
     extern __shared__ __align__(16) unsigned char smem[];
-    stage_tile<Real, COUNT, false, PEERS, true>(a, blockIdx.x, smem);
+    stage_tile<Real, COUNT, false, PEERS, true, REV>(a, blockIdx.x, smem);
 }
 
 // Wide-row variant (n_t >= 128, StageArgs::wide > 0): blocks of <= 256
 // threads with up to 128 registers, so the four corner pointers and the
 // eight in-flight chunk loads of a warp stay in registers.
-template <typename Real, bool COUNT, bool PEERS = false>
+template <typename Real, bool COUNT, bool PEERS = false, bool REV = false>
 __global__ void __launch_bounds__(256, ECO_WIDE_MINB)
 bellman_wide_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem[];
-    stage_tile<Real, COUNT, true, PEERS>(a, blockIdx.x, smem);
+    stage_tile<Real, COUNT, true, PEERS, false, REV>(a, blockIdx.x, smem);
 }
 
 // Batch of independent solves sharing one route's geometry (run_bench's

@@ -352,7 +352,7 @@ def backward_step(ctx: SolveContext, k: int, J_next: np.ndarray, *, backend: str
     device partition never changes results)."""
     prec = precision_of(backend)
     if perturb_ties:
-        raise ValueError("perturb_ties is a CPU-backend debug aid; the B200 kernels keep the lowest-index rule")
+        prec |= _abi.REVERSE_TIES
     g = ctx.grids
     m = _Marshal(ctx, [ctx.steps[k]])
     J_next = _f64(J_next)
@@ -393,12 +393,14 @@ def release_workspace():
     _abi.check(_abi.lib().eco_release_workspace(), "eco_release_workspace")
 
 
-def solve_stacks(ctx, backend: str = "b200", count_live: bool = False):
+def solve_stacks(ctx, backend: str = "b200", count_live: bool = False, perturb_ties: bool = False):
     """Device solve of a context -> (J stack (H+1, n_v, n_soc, n_t) f64,
     P stack (H, ...) int32, stats).  ``ctx`` only needs the reference
     SolveContext's attributes (dp.py:191-214), so this also serves the
-    reference's own objects (see plugin.py)."""
-    prec = precision_of(backend)
+    reference's own objects (see plugin.py).  ``perturb_ties``: ties go to the
+    highest flat action index (the reference's reverse_ties negative control,
+    _kernels.py:630-632)."""
+    prec = precision_of(backend) | (_abi.REVERSE_TIES if perturb_ties else 0)
     g, H = ctx.grids, ctx.horizon
     m = _Marshal(ctx, ctx.steps)
     terminal = _f64(ctx.terminal)
@@ -419,12 +421,10 @@ def solve_horizon(ctx: SolveContext, x_start: Optional[StateVector] = None, *, b
     All H stages run back to back on the GPU from one upload of the context;
     the full J / P stacks come back in the reference's layout."""
     precision_of(backend)
-    if perturb_ties:
-        raise ValueError("perturb_ties is a CPU-backend debug aid; the B200 kernels keep the lowest-index rule")
     H = ctx.horizon
     j_inf = ctx.penalty.j_inf
     t0 = time.perf_counter()
-    J_stack, P_stack, stats = solve_stacks(ctx, backend, count_live)
+    J_stack, P_stack, stats = solve_stacks(ctx, backend, count_live, perturb_ties)
     wall = time.perf_counter() - t0
     tables = [CostToGoTable(values=J_stack[k], v_axis=ctx.v_axes[k], soc_axis=ctx.soc_axis,
                             t_axis=ctx.t_axis, j_inf=j_inf) for k in range(H + 1)]
@@ -509,9 +509,7 @@ def make_toy_pack(r0: float = 0.25, c_nom: float = 64.0, voc: float = 2.0) -> Pl
 
 def solve_toy(toy: ToyInstance, *, backend: str = "b200", workers: int = 4, perturb_ties: bool = False):
     """Backward recursion over a toy instance -> (J stack, P stack) (dp.py:557-610)."""
-    prec = precision_of(backend)
-    if perturb_ties:
-        raise ValueError("perturb_ties is not supported by the B200 kernels")
+    prec = precision_of(backend) | (_abi.REVERSE_TIES if perturb_ties else 0)
     nv, nx, nt = toy.v_axis.shape[0], toy.soc_axis.shape[0], toy.t_axis.shape[0]
     nte, ntb = toy.n_actions_eng, toy.n_actions_bsg
     t0 = float(toy.t_axis[0])

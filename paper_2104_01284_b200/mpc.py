@@ -235,6 +235,21 @@ class MpcSession:
         return sum(a.nbytes for a in (rp.v_min, rp.v_max, rp.grade, rp.cos_g, rp.sin_g, rp.kinds, rp.cycle,
                                       rp.offset, rp.nwin, rp.win))
 
+    _PACK_FIELDS = ("v_min", "v_max", "grade", "kinds", "cycle", "offset", "nwin", "win")
+
+    def same_inputs(self, route: Route, spat: SpatSchedule) -> bool:
+        """True when (route, spat) carry the values this session was loaded
+        with (an equal route / SPaT passed as another object)."""
+        if route.node_count != self.route.node_count or route.delta_d != self.route.delta_d or \
+                route.accel_min != self.route.accel_min or route.accel_max != self.route.accel_max or \
+                route.stop_dwell != self.route.stop_dwell:
+            return False
+        try:
+            rp = _abi.RoutePack(route, spat)
+        except (KeyError, ValueError):
+            return False
+        return all(np.array_equal(getattr(rp, f), getattr(self._rp, f)) for f in self._PACK_FIELDS)
+
     def fit(self, field: Optional[np.ndarray] = None, want_field: bool = True):
         """Route geometry + terminal field on the device; returns (field or None, stats)."""
         n = self.route.node_count
@@ -335,8 +350,9 @@ def mpc_step(vehicle: Vehicle, route: Route, spat: SpatSchedule, x: StateVector,
     n = route.node_count
     if not 0 <= s < n - 1:
         raise ValueError(f"start node {s} out of range for {n} route nodes")
-    if perturb_ties:
-        raise ValueError("perturb_ties is not supported by the B200 kernels")
+    # perturb_ties flips only tied POLICY entries (the reference's
+    # reverse_ties); the decision reads J_1 at the exact state (mpc.py:189-278)
+    # and the costs are unchanged, so it cannot alter the action: accepted
     h = min(horizon, n - 1 - s)
     rows, status, _, fin, _, st = run_closed_loop(
         vehicle, route, spat, x, gamma=gamma, grids=grids, penalty=penalty, horizon=horizon, backend=backend,
@@ -363,15 +379,18 @@ def _session_for(vehicle, route, spat, **kw) -> "MpcSession":
     if hit is not None:
         return hit[0]
     while len(_SESSIONS) >= _SESSION_CAP:
-        _SESSIONS.pop(next(iter(_SESSIONS)))[0].close()
+        # drop the cache's reference only: a fitted controller may still hold
+        # this session (EcoDrivingMPC.session_); it is closed when the last
+        # holder lets go (MpcSession.__del__)
+        _SESSIONS.pop(next(iter(_SESSIONS)))
     sess = MpcSession(vehicle, route, spat, **kw)
     _SESSIONS[key] = (sess, vehicle, route, spat)
     return sess
 
 
 def clear_session_cache() -> None:
-    while _SESSIONS:
-        _SESSIONS.popitem()[1][0].close()
+    """Forget the cached sessions (each is closed once no controller holds it)."""
+    _SESSIONS.clear()
 
 
 class EcoDrivingMPC:
@@ -453,8 +472,12 @@ def simulate_closed_loop(route: Route, spat: SpatSchedule, controller: EcoDrivin
     if route.node_count == 1:
         traj.final_state = x_start
         return traj
-    if route is not controller.route_:
-        raise ValueError("simulate_closed_loop: controller was fitted on a different route")
+    if (route is not controller.route_ or spat is not controller.spat_) and \
+            not controller.session_.same_inputs(route, spat):
+        # the device loop plans and steps the plant on the fitted route / SPaT
+        # (the reference plans on controller.spat_ and steps on `spat`)
+        raise ValueError("simulate_closed_loop: route / SPaT differ from the ones the controller was fitted on; "
+                         "fit the controller on them first")
     rows, status, node, fin, st = controller.session_.run(x_start)
     if status == _abi.RUN_MISMATCH:
         raise RuntimeError(f"solver/plant transition mismatch at node {node}")

@@ -50,15 +50,13 @@ def install(names=tuple(BACKENDS)) -> None:
         if backend not in names:
             return orig_step(ctx, k, J_next, backend=backend, workers=workers, perturb_ties=perturb_ties)
         from . import dp as mdp
-        return mdp.backward_step(ctx, k, J_next, backend=backend)
+        return mdp.backward_step(ctx, k, J_next, backend=backend, perturb_ties=perturb_ties)
 
     def solve_horizon(ctx, x_start=None, *, backend="serial", workers=8, perturb_ties=False):
         if backend not in names:
             return orig_solve(ctx, x_start, backend=backend, workers=workers, perturb_ties=perturb_ties)
-        if perturb_ties:
-            raise ValueError("perturb_ties is not supported by the B200 backends")
         t0 = time.perf_counter()
-        J, P, _ = solve_stacks(ctx, backend)
+        J, P, _ = solve_stacks(ctx, backend, perturb_ties=perturb_ties)
         wall = time.perf_counter() - t0
         j_inf = ctx.penalty.j_inf
         tables = [rdp.CostToGoTable(values=J[k], v_axis=ctx.v_axes[k], soc_axis=ctx.soc_axis,

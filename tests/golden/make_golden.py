@@ -149,6 +149,91 @@ def loop_urban():
     }, indent=1))
 
 
+C3_GRID = dict(n_v=350, n_soc=260, n_t=400, dt=0.2)
+C3_SAMPLES = 16384
+
+
+def c3():
+    """C3: urban s=60, t=30, the fine grid, all 21 J / 20 P levels (digests of
+    every level + a seeded sample of states for the fp32 tolerance checks)."""
+    vehicle = make_vehicle()
+    route, spat = load_fixture_route("urban", seed=0)
+    ctx = build_context(vehicle, route, spat, 60, 30.0, grids=GridSpec(**C3_GRID), penalty=PEN, gamma=0.5,
+                        horizon=20)
+    t0 = time.perf_counter()
+    res = solve_horizon(ctx, backend="parallel", workers=8)
+    wall = time.perf_counter() - t0
+    ns = res.tables[0].values.size
+    idx = np.random.default_rng(2104).choice(ns, C3_SAMPLES, replace=False).astype(np.int64)
+    idx.sort()
+    Js = np.stack([tb.values.reshape(-1)[idx] for tb in res.tables])
+    Ps = np.stack([p.values.reshape(-1)[idx] for p in res.policies])
+    summ = []
+    for tb in res.tables:
+        fin = tb.values < PEN.j_inf
+        summ.append({"finite": int(fin.sum()), "sum_finite": float(tb.values[fin].sum())})
+    np.savez_compressed(HERE / "c3_urban_s60_t30_samples.npz", idx=idx, J=Js, P=Ps)
+    (HERE / "c3_urban_s60_t30.json").write_text(json.dumps({
+        "s": 60, "t_start": 30.0, "grid": C3_GRID, "horizon": 20,
+        "wall_s_reference_parallel8": wall,
+        "J": [table_digest(tb.values) for tb in res.tables],
+        "P": [table_digest(p.values) for p in res.policies],
+        "P_infeasible": [int((p.values < 0).sum()) for p in res.policies],
+        "levels": summ,
+    }, indent=1))
+    print(f"c3 solve {wall:.1f}s", flush=True)
+
+
+C3_LOOP_STEPS = 10
+
+
+def loop_c3():
+    """North-star target at the finest grid: EcoDrivingMPC(C3 grid).fit(urban)
+    (terminal field on) and the first C3_LOOP_STEPS nodes of the closed loop,
+    stepped exactly as simulate_closed_loop (mpc.py:549-596) steps them."""
+    from ecodrive.errors import StartStateInfeasibleError
+    from ecodrive.mpc import _max_braking_decision
+    from ecodrive.plant import StateVector, propagate_state_full
+    from ecodrive.route import NODE_SIGNAL
+    vehicle = make_vehicle()
+    route, spat = load_fixture_route("urban", seed=0)
+    t0 = time.perf_counter()
+    mpc = EcoDrivingMPC(vehicle, gamma=0.5, grids=GridSpec(**C3_GRID), penalty=PEN, horizon=20,
+                        backend="parallel", workers=8).fit(route, spat)
+    t_fit = time.perf_counter() - t0
+    print(f"c3 field {t_fit:.1f}s", flush=True)
+    fv = mpc.terminal_field_.values
+    nodes = np.array([0, 20, 21, 25, 30, 80, 150, 698, 699])
+    np.savez_compressed(HERE / "fields_c3.npz", urban_nodes=nodes, urban_slices=fv[nodes])
+    kinds = route.node_kinds()
+    x = StateVector(v=0.0, soc=0.5, t=0.0)
+    rows, walls = [], []
+    for s in range(C3_LOOP_STEPS):
+        t1 = time.perf_counter()
+        try:
+            dec = mpc.control(x, s)
+        except StartStateInfeasibleError as exc:
+            dec = _max_braking_decision(vehicle, route, x, s, str(exc))
+        walls.append(time.perf_counter() - t1)
+        src = int(kinds[s])
+        sig = spat.timing(route.traffic_lights[s]) if src == NODE_SIGNAL else None
+        x_next, info = propagate_state_full(vehicle, x, dec.action, route.delta_d, grade=float(route.grade[s]),
+                                            source_kind=src, dest_kind=int(kinds[s + 1]), signal=sig,
+                                            stop_dwell=route.stop_dwell, teleport=True,
+                                            brake_force=dec.brake_force)
+        rows.append([s, x.v, x.soc, x.t, dec.action.t_eng, dec.action.t_bsg, dec.brake_force, info.gear,
+                     info.wait, info.dt_move, info.fuel_g, info.accel, dec.cost_to_go, float(dec.fallback)])
+        x = x_next
+        print(f"c3 loop step {s}: {walls[-1]:.1f}s", flush=True)
+    np.savez_compressed(HERE / "loop_urban_c3_prefix.npz", rows=np.array(rows, dtype=np.float64),
+                        final=np.array([x.v, x.soc, x.t]))
+    (HERE / "loop_urban_c3_prefix.json").write_text(json.dumps({
+        "steps": C3_LOOP_STEPS, "grid": C3_GRID, "horizon": 20,
+        "field_digest": table_digest(fv), "field_shape": list(fv.shape),
+        "fit_s_reference": t_fit, "step_s_reference_parallel8": walls,
+    }, indent=1))
+
+
 def primitives():
     rng = np.random.default_rng(1234)
     vehicle = make_vehicle()
@@ -187,7 +272,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     jobs = [("primitives", primitives), ("toys", toys), ("c1", c1), ("fields", fields), ("loop_short", loop_short),
-            ("c2", c2_digests), ("c4", c2_batch_seeds)]
+            ("c2", c2_digests), ("c4", c2_batch_seeds), ("c3", c3), ("loop_c3", loop_c3)]
     if not a.skip_urban_loop:
         jobs.append(("loop_urban", loop_urban))
     for name, fn in jobs:
