@@ -1,40 +1,44 @@
 #!/usr/bin/env python3
 """Benchmark: receding-horizon eco-driving DP on B200 (BASELINE.json metric).
 
-Workload at N=1 (BASELINE.json configs[1]): closed-loop MPC over
-the synthetic 700-node urban route with SPaT (5 signals, 2 stop signs),
-default grid (35 x 26 x 40 states, 23 x 30 actions), H = 20, gamma = 0.5,
-x0 = (0, 0.5, 0), terminal field on.  One *step* = one full closed-loop run:
-EcoDrivingMPC.fit (route geometry + signal-free terminal field, 699 (v,soc)
-sweeps) followed by 699 receding-horizon solves (13,790 Bellman stages), the
-exact-state argmin and the plant step at every node.
+Default workload at N=1 (BASELINE.json configs[2], SURVEY §8d C3 — the largest
+single-GPU configuration, the north star's "finest named grid"): one
+receding-horizon DP solve of the synthetic 700-node urban route with SPaT at
+urban node s = 60, clock t = 30 s, fine grid 350 x 260 x 400 states (dt =
+0.2 s) x 23 x 30 controls, H = 20, gamma = 0.5.  One *step* = one solve:
+the J-independent transition geometry of the 20 spatial steps (the
+reference's stage 1) + 20 Bellman stage sweeps (5.02e11 dense updates).
 
-  value   dense Bellman updates/s over the step, device-timed (CUDA events on
-          the launch stream), route/vehicle already uploaded (session built);
-  e2e     the same metric through the public API (EcoDrivingMPC.fit +
-          simulate_closed_loop) with host inputs and host outputs, including
-          allocation, H2D and the D2H of the trajectory and terminal field.
-
-N > 1 GPUs: the closed loop is sequential along the route, so ranks run
-independent replicas ("replicas only"): value = sum of updates /
-max over ranks of the device time.
+  value   dense Bellman updates/s, device time of the solves (CUDA events on
+          the solver's stream around the device work of each call: inputs
+          already in HBM, outputs left there), summed over the K steps;
+  e2e     the same metric through the public API (solve_horizon -> a
+          SolveResult with all 21 f64 J levels and 20 int32 policy levels on
+          the host) with the host context in and the 9 GB of tables out,
+          wall-clocked with a device synchronize on both sides.
 
 `--impl reference`: the reference algorithm's CPU implementation (the pinned
-C restatement in oracle/, all host threads) on a bounded sample of the same
-workload: fit + the first M receding-horizon steps.
+C restatement in oracle/, kind "port", all host threads) on the SAME C3
+solve: step i runs stage H-1-(i mod H) of the horizon, chained from the
+terminal level, so K = 20 timed steps are exactly one full C3 solve.
 
-Other workloads (`--workload`; the default line is C2):
+N > 1 GPUs: independent replicas of the solve ("replicas only" for C3;
+the slab-partitioned single grid is C5): value = sum over ranks / max time.
+
+Other workloads (`--workload`):
+  c2  BASELINE configs[1]: the closed-loop MPC over the urban route, default
+      grid 35 x 26 x 40 x 23 x 30, H = 20, terminal field on; one step = fit +
+      699 receding-horizon solves (13,790 stages).  Replicas for N > 1.
   c4  BASELINE configs[3]: 4096 independent urban scenarios (route seed i,
       bench_schedule(route_i, 20, 1, seed=i)[0]), C2 grid, H = 20, no terminal
       field; sharded over ranks in contiguous blocks (strong scaling, no
       inter-GPU communication).  One step = one batch solve of the shard.
-  c3  BASELINE configs[2]: one receding-horizon solve on the fine grid
-      350 x 260 x 400 (dt = 0.2 s), urban s = 60, t = 30, H = 20.  Replicas
-      for N > 1 (the slab-partitioned variant is C5).
   c5  BASELINE configs[4]: the C3 solve with its speed planes split into N
       slabs, one per GPU (strong scaling); after every stage the slabs are
       exchanged (--exchange p2p: NVLink stores from the stage kernel's
       epilogue + GPU flag barrier; nccl: grouped ncclBroadcast).
+  n1  the north-star Target: the closed loop at the C3 grid (fit with the
+      terminal field + the first --loop-steps receding-horizon solves).
 """
 
 from __future__ import annotations
@@ -236,10 +240,7 @@ def run_ours(args, rank, world, local_rank):
         peak /= 2.0     # B200: FP64 at half the FP32 rate
     sweep_avg_s = sweep_ms / args.steps / 1e3
     achieved = FLOPS_PER_LIVE * live / sweep_avg_s / 1e12
-    traffic = None
-    tf = ROOT / "profiles" / "stage_kernel_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"c2_{args.precision}")
+    traffic, tsrc = measured_traffic(f"c2_{args.precision}")
     launches_per_step = rst["kernel_launches"] + fst["kernel_launches"]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -260,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": per_step * args.steps * world / (e2e_ms / 1e3), "unit": UNIT,
                 "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "fp32", "kernel": "bellman_stage_kernel", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
                      "peak_source": f"CUDA-core FP32 = 2 x 128 x {props.multi_processor_count} SMs x "
                                     f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)"
                                     + (" / 2 for FP64" if args.precision == "fp64" else ""),
@@ -308,7 +309,9 @@ def cpu_baseline(budget_s: float) -> dict:
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    if args.workload in ("c3", "c4", "c5"):
+    if args.workload == "c3":
+        return run_reference_c3(args, world)
+    if args.workload in ("c4", "c5"):
         return run_reference_other(args, world)
     budget = args.cpu_seconds
     probe = cpu_sample(3)
@@ -356,7 +359,7 @@ def _max_over_ranks(dist, ms):
     return float(t.item())
 
 
-def _roofline(args, local_rank, live, sweep_s, kernel):
+def _roofline(args, local_rank, live, sweep_s, kernel, traffic=None, traffic_src=None, algorithmic_bytes=None):
     import torch
     peaks = measured_peaks()
     props = torch.cuda.get_device_properties(local_rank)
@@ -365,15 +368,16 @@ def _roofline(args, local_rank, live, sweep_s, kernel):
     if args.precision == "fp64":
         peak /= 2.0
     achieved = FLOPS_PER_LIVE * live / sweep_s / 1e12
-    traffic = None
-    tf = ROOT / "profiles" / "stage_kernel_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"{args.workload}_{args.precision}")
-    return {"bound": "fp32", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "peak_source": f"CUDA-core FP32 = 2 x 128 x {props.multi_processor_count} SMs x {sm_max:.0f} MHz"
-                           + (" / 2 for FP64" if args.precision == "fp64" else ""),
-            "algorithmic": f"{FLOPS_PER_LIVE} flop x {live} live gathers / summed sweep time"}
+    out = {"bound": "fp32", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+           "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+           "peak_source": f"CUDA-core FP32 = 2 x 128 x {props.multi_processor_count} SMs x {sm_max:.0f} MHz"
+                          + (" / 2 for FP64" if args.precision == "fp64" else "")
+                          + " (FP32 is not in MEASURED_PEAKS.json; its sm_max_mhz is)",
+           "algorithmic": f"{FLOPS_PER_LIVE} flop x {live} live gathers / summed sweep time (all stage launches "
+                          f"of a solve)"}
+    if algorithmic_bytes:
+        out["algorithmic_bytes_per_launch"] = int(algorithmic_bytes)
+    return out
 
 
 def c4_inputs(n):
@@ -456,7 +460,8 @@ def run_c4(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "e2e": {"value": total_dense / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": int(res.stats["h2d_bytes"]), "d2h_bytes_per_step": int(res.stats["d2h_bytes"])},
-        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_batch_kernel"),
+        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_batch_kernel",
+                              *measured_traffic(f"c4_{args.precision}")),
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
@@ -491,12 +496,40 @@ def c4_cpu_baseline(budget_s):
             "ms_per_solve": 1e3 * s["seconds"] / n}
 
 
+C3_WORKLOAD = ("C3: one receding-horizon DP solve, urban 700-node route with SPaT, node s=60, t=30 s, fine grid "
+               "350x260x400 states (dt=0.2 s) x 23x30 controls, H=20, gamma=0.5 (5.02e11 dense updates per solve)")
+C3_CONFIG = {"workload": C3_WORKLOAD,
+             "l2": "each level (145.6 MB f32 / 291 MB f64) exceeds the 126 MB L2: inputs larger than L2, no flush"}
+
+
 def c3_context(H=20):
     from paper_2104_01284_b200 import (GridSpec, PenaltyConfig, build_context, load_fixture_route, make_vehicle)
     route, spat = load_fixture_route("urban", seed=0)
     grids = GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2)
     return build_context(make_vehicle(), route, spat, 60, 30.0, grids=grids, penalty=PenaltyConfig(), gamma=0.5,
                          horizon=H)
+
+
+def so_digest() -> str:
+    import hashlib
+    from paper_2104_01284_b200 import _abi
+    return hashlib.sha256(_abi.library_path().read_bytes()).hexdigest()[:16]
+
+
+def measured_traffic(key: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture of THIS build (profiles/traffic.json records the library digest
+    it was taken on); None when the capture belongs to another build."""
+    tf = ROOT / "profiles" / "traffic.json"
+    if not tf.exists():
+        return None, "no capture committed"
+    d = json.loads(tf.read_text())
+    ent = d.get(key)
+    if not ent:
+        return None, f"no capture for {key}"
+    if ent.get("so_digest") != so_digest():
+        return None, f"capture {ent.get('file')} was taken on another build ({ent.get('so_digest')})"
+    return ent["dram_bytes"], ent.get("file")
 
 
 def run_c3(args, rank, world, local_rank):
@@ -509,59 +542,133 @@ def run_c3(args, rank, world, local_rank):
     for _ in range(args.warmup):
         solve_stacks(ctx, backend)
     live = solve_stacks(ctx, backend, count_live=True)[2]["live_updates"]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     dev_ms, sweep_ms, dense, launches = 0.0, 0.0, 0, 0
     with ClockSampler(local_rank) as clk:
+        barrier()
+        w0 = time.perf_counter()
         for _ in range(args.steps):
-            st = solve_stacks(ctx, backend)[2]
+            J, P, st = solve_stacks(ctx, backend)
+            del J, P
             dev_ms += st["device_ms"]
             sweep_ms += st["dominant_ms"]
             dense += st["dense_updates"]
             launches += st["kernel_launches"]
+        barrier()
+        wall_ms = (time.perf_counter() - w0) * 1e3
     t_max = _max_over_ranks(dist, dev_ms)
-    if dist is not None:
-        dist.barrier()
+    sweep_max = _max_over_ranks(dist, sweep_ms)
+    # e2e: the public API, host context in, SolveResult (all levels) out
+    res = solve_horizon(ctx, backend=backend)
+    del res
+    barrier()
     a0 = time.perf_counter()
     for _ in range(args.steps):
         res = solve_horizon(ctx, backend=backend)
+        del res           # the previous result's pinned blocks go back to the pool
+    barrier()
     e2e_ms = _max_over_ranks(dist, (time.perf_counter() - a0) * 1e3)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return None
-    ns = ctx.grids.n_v * ctx.grids.n_soc * ctx.grids.n_t
+    g = ctx.grids
+    ns = g.n_v * g.n_soc * g.n_t
+    traffic, tsrc = measured_traffic(f"c3_{args.precision}")
     out = {
         "metric": METRIC, "value": dense * world / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (urban route seed 0)",
-        "config": {"workload": "C3: one receding-horizon solve, fine grid 350x260x400 (dt=0.2) x 23x30, urban "
-                               "s=60 t=30, H=20 (geometry of the 20 steps + 20 stage sweeps per step)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "levels of 291 MB exceed L2; no flush", "precision": args.precision,
-                   "timing": "device time per solve from CUDA events on the solver's stream (sum over steps)"},
-        "ms_per_solve": t_max / args.steps, "sweep_ms_per_solve": sweep_ms / args.steps,
+        "data": "synthetic (reference fixture generators: urban route seed 0, synthetic 48V P0 vehicle)",
+        "config": dict(C3_CONFIG),
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU", "precision": args.precision,
+        "timing": "value: CUDA events on the solver's stream around each solve's device work (geometry of the 20 "
+                  "steps + 20 stage sweeps + output conversion), summed over the K steps; wall clock of the same "
+                  "K steps with sync on both sides in wall_ms (includes the 291 MB terminal H2D per call)",
+        "wall_ms": wall_ms,
+        "ms_per_solve": t_max / args.steps, "sweep_ms_per_solve": sweep_max / args.steps,
         "dense_updates_per_step": dense / args.steps, "live_updates_per_step": live,
         "gpu_launches": int(launches),
         "e2e": {"value": dense * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
-                "h2d_bytes_per_step": int(ns * 8 + 20 * (4 * 8 * ctx.grids.n_t)),
-                "d2h_bytes_per_step": int(21 * ns * 8 + 20 * ns * 4)},
-        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_stage_kernel"),
+                "h2d_bytes_per_step": int(ns * 8 + 20 * (g.n_v * 8 + g.n_t * (1 + 1 + 8 + 8))),
+                "d2h_bytes_per_step": int(21 * ns * 8 + 20 * ns * 4),
+                "api": "paper_2104_01284_b200.solve_horizon(ctx, backend) -> SolveResult (pinned output pool)"},
+        "roofline": _roofline(args, local_rank, live, sweep_max / args.steps / 1e3, "bellman_wide_kernel",
+                              traffic, tsrc, algorithmic_bytes=ns * 4 + 3 * ns * 4),
         "clocks": clk.summary(),
     }
-    del res
     if not args.no_cpu_baseline and world == 1:
-        from oracle import oracle as O
-        c = c3_context(H=1)
-        t0 = time.perf_counter()
-        O.solve_context(c, parallel=True)
-        sec = time.perf_counter() - t0
-        ups = ns * ctx.grids.n_t_eng * ctx.grids.n_t_bsg
-        out["cpu_baseline"] = {"value": ups / sec, "unit": UNIT, "cores": O.threads_available(), "kind": "port",
-                               "sample": "one C3 Bellman stage (the last of the horizon) with the oracle's "
-                                         "two-stage sweep on all host threads", "seconds": sec}
+        out["cpu_baseline"] = c3_cpu_baseline(args.cpu_seconds)
     if dist is not None:
         dist.destroy_process_group()
     return out
+
+
+def c3_stage_chain(ctx, n_steps, threads, J=None, k=None):
+    """Oracle stages of the C3 solve, chained: stage H-1 from the terminal,
+    then H-2 from its output, ... (restarting at the terminal after stage 0).
+    Returns (per-stage seconds, per-stage dense updates, state)."""
+    from oracle import oracle as O
+    g = ctx.grids
+    ups = g.n_v * g.n_soc * g.n_t * g.n_t_eng * g.n_t_bsg
+    H = ctx.horizon
+    times = []
+    if J is None:
+        J, k = np.asarray(ctx.terminal, dtype=np.float64), H - 1
+    for _ in range(n_steps):
+        t0 = time.perf_counter()
+        Jk, _, _ = O.sweep(ctx, k, J, parallel=True, threads=threads)
+        times.append(time.perf_counter() - t0)
+        J, k = Jk, k - 1
+        if k < 0:
+            J, k = np.asarray(ctx.terminal, dtype=np.float64), H - 1
+    return times, [ups] * n_steps, (J, k)
+
+
+def c3_cpu_baseline(budget_s):
+    from oracle import oracle as O
+    ctx = c3_context()
+    threads = O.threads_available()
+    t1, _, st = c3_stage_chain(ctx, 1, threads)
+    n = int(max(1, min(ctx.horizon - 1, budget_s / max(t1[0], 1e-3))))
+    times, ups, _ = c3_stage_chain(ctx, n, threads, *st)
+    times = t1 + times
+    ups = [ups[0]] * len(times)
+    return {"value": sum(ups) / sum(times), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"the first {len(times)} of the 20 stages of the same C3 solve, chained from the terminal "
+                      f"level (oracle/eco_oracle.c two-stage sweep, {threads} OpenMP threads)",
+            "seconds": sum(times), "ms_per_solve_est": 1e3 * sum(times) / len(times) * ctx.horizon}
+
+
+def run_reference_c3(args, world):
+    """--impl reference for the default C3 line: the oracle port on the same
+    solve, one stage per step, chained (K = 20 steps = the whole solve)."""
+    from oracle import oracle as O
+    ctx = c3_context()
+    threads = O.threads_available()
+    _, _, st = c3_stage_chain(ctx, args.warmup, threads)        # warm-up: the first W stages
+    times, ups, _ = c3_stage_chain(ctx, args.steps, threads)    # timed: restart at the terminal
+    value = sum(ups) / sum(times)
+    H = ctx.horizon
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference fixture generators: "
+        "urban route seed 0, synthetic 48V P0 vehicle)", "impl": "reference", "config": dict(C3_CONFIG),
+        "ms_per_solve": 1e3 * sum(times) / len(times) * H,
+        "stages_timed": len(times),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"the C3 solve itself: step i = stage {H - 1}-(i mod {H}) chained from the "
+                                   f"terminal level, so the {args.steps} timed steps cover "
+                                   f"{args.steps / H:g} full H={H} solve(s) (oracle/eco_oracle.c, the pinned C "
+                                   f"restatement of the reference's two-stage numba sweep, {threads} OpenMP threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
 
 
 def run_reference_other(args, world):
@@ -664,7 +771,75 @@ def run_c5(args, rank, world, local_rank):
         "e2e": {"value": dense * args.steps / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": int(ns * 8), "d2h_bytes_per_step": int(res.P.nbytes)},
         "roofline": _roofline(args, local_rank, live_all / world, sweep_max / args.steps / 1e3,
-                              "bellman_wide_kernel"),
+                              "bellman_wide_kernel", *measured_traffic(f"c5_{args.precision}")),
+        "clocks": clk.summary(),
+    }
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+
+def run_n1(args, rank, world, local_rank):
+    """North-star Target: the receding-horizon closed loop at the C3 grid.
+    EcoDrivingMPC.fit (chunked terminal field over the 700-node route) once,
+    then each step = the first --loop-steps nodes of the closed loop from
+    x0 = (0, 0.5, 0): per node a full H=20 C3 solve (ring of plan slots), the
+    exact-state decision and the plant step, all on the device."""
+    import torch
+    from paper_2104_01284_b200 import GridSpec, PenaltyConfig, StateVector, load_fixture_route, make_vehicle
+    from paper_2104_01284_b200.mpc import MpcSession
+    dist = _dist_init(world, local_rank)
+    backend = "b200-fp64" if args.precision == "fp64" else "b200"
+    route, spat = load_fixture_route("urban", seed=0)
+    grids = GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2)
+    sess = MpcSession(make_vehicle(), route, spat, gamma=0.5, grids=grids, penalty=PenaltyConfig(), horizon=20,
+                      backend=backend)
+    _, fst = sess.fit(want_field=False)
+    x0 = StateVector(0.0, 0.5, 0.0)
+    M = args.loop_steps
+    for _ in range(args.warmup):
+        sess.run(x0, 0, M)
+    live = sess.run(x0, 0, M, count_live=True)[4]["live_updates"]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dev_ms, sweep_ms, dense, launches = 0.0, 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for _ in range(args.steps):
+            rows, status, _, fin, st = sess.run(x0, 0, M)
+            assert status == 0 and len(rows) == M
+            dev_ms += st["device_ms"]
+            sweep_ms += st["dominant_ms"]
+            dense += st["dense_updates"]
+            launches += st["kernel_launches"]
+        barrier()
+    t_max = _max_over_ranks(dist, dev_ms)
+    sess.close()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    out = {
+        "metric": METRIC, "value": dense * world / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (reference fixture generators: urban route seed 0, synthetic 48V P0 vehicle)",
+        "config": {"workload": f"N1 (north-star Target): closed-loop MPC on the urban route at the C3 grid "
+                               f"350x260x400 (dt=0.2) x 23x30, H=20, terminal field on; one step = the first {M} "
+                               f"nodes from x0=(0, 0.5, 0) (one full C3 solve + decision + plant step per node)",
+                   "l2": "levels of 145.6 MB exceed L2; no flush"},
+        "precision": args.precision,
+        "fit_ms": fst["device_ms"], "fit_field_sweep_ms": fst["dominant_ms"],
+        "ms_per_solve": t_max / args.steps / M, "sweep_ms_per_solve": sweep_ms / args.steps / M,
+        "live_updates_per_step": live, "gpu_launches": int(launches),
+        "final_state": [float(x) for x in fin],
+        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_wide_kernel",
+                              *measured_traffic(f"c3_{args.precision}")),
         "clocks": clk.summary(),
     }
     if dist is not None:
@@ -681,9 +856,10 @@ def main():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5", "n1"], default="c3")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p", help="C5 slab exchange")
     ap.add_argument("--scenarios", type=int, default=4096, help="C4 batch size (all ranks together)")
+    ap.add_argument("--loop-steps", type=int, default=20, help="n1: closed-loop nodes per step")
     args = ap.parse_args()
     rank, world, local_rank = env_rank()
     if world != args.gpus and world == 1:
@@ -696,6 +872,8 @@ def main():
         out = run_c3(args, rank, world, local_rank)
     elif args.workload == "c5":
         out = run_c5(args, rank, world, local_rank)
+    elif args.workload == "n1":
+        out = run_n1(args, rank, world, local_rank)
     else:
         out = run_ours(args, rank, world, local_rank)
     if out is not None:

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ECO_ABI_VERSION 5
+#define ECO_ABI_VERSION 6
 
 #define ECO_MAX_GEARS 16
 #define ECO_MAX_AXIS 32
@@ -194,6 +194,13 @@ int32_t eco_device_count(void);
  * This frees it. */
 int32_t eco_release_workspace(void);
 
+/* Page-locked host buffers for solver outputs: J / P stacks written into
+ * them arrive by direct DMA (no staging copy), and level by level while the
+ * remaining stages still sweep.  Any output pointer may also be ordinary
+ * pageable memory. */
+int32_t eco_host_alloc(uint64_t bytes, void** out);
+int32_t eco_host_free(void* p);
+
 /* One backward Bellman step (backward_step, dp.py:365-404).  J_next, J_out
  * are (n_v, n_soc, n_t) f64, P_out int32.  tables may be NULL (plant path). */
 int32_t eco_bellman_step(const EcoPlant* plant, const EcoProblem* prob,
@@ -332,6 +339,16 @@ int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant,
                        int32_t H, const double* terminal, double* J_stack,
                        int32_t* P_slab, int32_t count_live, EcoStats* stats);
 int32_t eco_slab_destroy(EcoSlab* slab);
+/* The slab decomposition of nranks ranks emulated on ONE GPU (tests of the
+ * exchange where fewer GPUs than ranks are available): one launch per stage
+ * covers every rank's tiles, each rank keeps its own replica of the levels,
+ * filled through the same peer-store epilogue and local copy-1 rebuild as the
+ * multi-GPU path.  J_stacks receives every rank's replica, (nranks, H + 1,
+ * n_v, n_soc, n_t) f64; P_stack (nullable) the policy stack assembled from
+ * the slabs.  nranks <= 8. */
+int32_t eco_slab_emulate(int32_t nranks, const int32_t* bounds, int32_t precision, const EcoPlant* plant,
+                         const EcoProblem* prob, const EcoStepPlan* plans, int32_t H, const double* terminal,
+                         double* J_stacks, int32_t* P_stack, EcoStats* stats);
 
 #ifdef __cplusplus
 }

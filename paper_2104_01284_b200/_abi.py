@@ -21,7 +21,7 @@ MAX_GEARS = 16
 MAX_AXIS = 32
 MAX_MAP = MAX_AXIS * MAX_AXIS
 MAX_WINDOWS = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 XCHG_P2P, XCHG_NCCL = 0, 1
 SLAB_INFO_BYTES = 256
 
@@ -225,6 +225,8 @@ def _declare(lib):
         "eco_last_error": (C.c_char_p, []),
         "eco_device_count": (_I, []),
         "eco_release_workspace": (_I, []),
+        "eco_host_alloc": (_I, [C.c_uint64, P(C.c_void_p)]),
+        "eco_host_free": (_I, [C.c_void_p]),
         "eco_bellman_step": (_I, [P(EcoPlant), P(EcoProblem), P(EcoStepPlan), P(EcoStage1Tables),
                                   _PD, _PD, _PI, _I, _I, P(EcoStats)]),
         "eco_solve_horizon": (_I, [P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI, _I, _I,
@@ -249,6 +251,8 @@ def _declare(lib):
         "eco_slab_solve": (_I, [C.c_void_p, P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI, _I,
                                 P(EcoStats)]),
         "eco_slab_destroy": (_I, [C.c_void_p]),
+        "eco_slab_emulate": (_I, [_I, _PI, _I, P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI,
+                                  P(EcoStats)]),
         "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _I, C.c_void_p, _PI, _PD, _PD, _PI,
                                  P(EcoStats)]),
     }
@@ -287,3 +291,75 @@ def check(status: int, what: str):
     if status == ERR_ARG:
         raise ValueError(f"{what}: {msg}")
     raise NativeLibraryError(f"{what} failed (status {status}): {msg}")
+
+
+# ------------------------------------------------------------ pinned outputs
+
+class _PinnedBuf:
+    """One page-locked block exposed as a numpy array (via the array
+    interface); returns the block to its pool when the last view dies."""
+
+    def __init__(self, pool, ptr: int, cap: int, shape, dtype):
+        self._pool, self._ptr, self._cap = pool, ptr, cap
+        self.__array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
+                                    "typestr": np.dtype(dtype).str, "version": 3}
+
+    def __del__(self):
+        try:
+            self._pool._give_back(self._ptr, self._cap)
+        except Exception:       # interpreter shutdown
+            pass
+
+
+class PinnedPool:
+    """Recycled page-locked host blocks for solver outputs (eco_host_alloc).
+
+    Tables written into them arrive by direct DMA, overlapped level by level
+    with the remaining sweep (eco_solve_horizon), instead of through a staging
+    copy into pageable numpy memory.  Arrays handed out are ordinary numpy
+    arrays; when a result is dropped its block goes back to the pool.  Idle
+    blocks beyond ``keep_bytes`` are unpinned."""
+
+    def __init__(self, keep_bytes: int = 24 << 30):
+        import threading
+        self._lock = threading.Lock()
+        self._free = []               # (capacity, ptr)
+        self._keep = keep_bytes
+
+    def array(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        need = max(nbytes, 1)
+        with self._lock:
+            best = None
+            for i, (cap, ptr) in enumerate(self._free):
+                if need <= cap <= 2 * need + (64 << 20) and (best is None or cap < self._free[best][0]):
+                    best = i
+            blk = self._free.pop(best) if best is not None else None
+        if blk is None:
+            cap = (need + (2 << 20) - 1) & ~((2 << 20) - 1)
+            out = C.c_void_p()
+            check(lib().eco_host_alloc(cap, C.byref(out)), "eco_host_alloc")
+            blk = (cap, out.value)
+        return np.asarray(_PinnedBuf(self, blk[1], blk[0], shape, dtype))
+
+    def _give_back(self, ptr: int, cap: int):
+        with self._lock:
+            self._free.append((cap, ptr))
+            total = sum(c for c, _ in self._free)
+            drop = []
+            while total > self._keep and self._free:
+                c, p = self._free.pop(0)
+                total -= c
+                drop.append(p)
+        for p in drop:
+            lib().eco_host_free(p)
+
+    def clear(self):
+        with self._lock:
+            drop, self._free = self._free, []
+        for _, p in drop:
+            lib().eco_host_free(p)
+
+
+PINNED = PinnedPool()

@@ -5,6 +5,7 @@
 // internal representation (Real, infeasible == +inf).  No CPU compute path.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -12,6 +13,7 @@
 #include <string>
 #include <algorithm>
 #include <memory>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <stdexcept>
@@ -167,13 +169,47 @@ struct EventTimer {
     }
 };
 
+// Host memcpy spread over up to 16 threads (large pinned <-> pageable copies:
+// one core moves ~10 GB/s, the copy engines ~50).
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    if (n < (size_t(8) << 20)) {
+        std::memcpy(d, s, n);
+        return;
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nthr = (int)std::max(1u, std::min(16u, hw ? hw : 1u));
+    std::vector<std::thread> th;
+    const size_t per = ((n + nthr - 1) / nthr + 4095) & ~size_t(4095);
+    for (int t = 0; t < nthr; ++t) {
+        const size_t a = (size_t)t * per;
+        if (a >= n) break;
+        const size_t m = std::min(per, n - a);
+        th.emplace_back([=] { std::memcpy(d + a, s + a, m); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// Page-locked host memory (cudaHostAlloc, or registered): the copy engines
+// DMA straight into it, so a device -> host copy needs no staging.
+inline bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();   // pageable memory may report an error on old drivers
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 // Large device -> pageable-host copies (the J / P stacks of fine-grid solves,
 // batch tables): double-buffered pinned staging; chunk i's host-side copy is
 // spread over threads (first-touching the destination in parallel) while
-// chunk i + 1's DMA runs.  Completes before returning.
+// chunk i + 1's DMA runs.  Completes before returning.  A pinned destination
+// (eco_host_alloc, the Python pinned pool) takes one direct DMA instead.
 void download_big(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     constexpr size_t kChunk = size_t(64) << 20;
-    if (bytes < (size_t(32) << 20) || std::getenv("ECO_PLAIN_D2H")) {
+    if (bytes < (size_t(32) << 20) || std::getenv("ECO_PLAIN_D2H") || host_pinned(dst)) {
         if (bytes) ECO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
         ECO_CUDA(cudaStreamSynchronize(st));
         return;
@@ -188,19 +224,7 @@ void download_big(void* dst, const void* src, size_t bytes, cudaStream_t st) {
             ECO_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
         }
     }
-    const unsigned hw = std::thread::hardware_concurrency();
-    const int nthr = (int)std::max(1u, std::min(16u, hw ? hw : 1u));
-    auto host_copy = [&](char* d, const char* s, size_t n) {
-        std::vector<std::thread> th;
-        const size_t per = (n + nthr - 1) / nthr;
-        for (int t = 0; t < nthr; ++t) {
-            const size_t a = (size_t)t * per;
-            if (a >= n) break;
-            const size_t m = std::min(per, n - a);
-            th.emplace_back([=] { std::memcpy(d + a, s + a, m); });
-        }
-        for (auto& x : th) x.join();
-    };
+    auto host_copy = [&](char* d, const char* s, size_t n) { parallel_memcpy(d, s, n); };
     char* out = static_cast<char*>(dst);
     const char* in = static_cast<const char*>(src);
     int prev = -1;
@@ -267,10 +291,12 @@ struct Geometry {
     int plo = 0, phi = -1;                  // tiles of planes [plo, phi) ordered first (slab solves)
     int tj_pref = 0, slices_pref = 0;       // tile shape overrides (0: defaults); the batch prefers 4 x 8
 
+    // grow-only: rebuilding a smaller set of plans (field chunks, ring
+    // slots) keeps the allocation
     void alloc(int P, int nv, int U) {
         const size_t np = (size_t)P * nv * U;
-        count.alloc((size_t)P * nv); row_off.alloc((size_t)P * nv); gmax.alloc(4);
-        u.alloc(np); dt.alloc(np); c1d.alloc(np); pbat.alloc(np); act.alloc(np);
+        count.ensure((size_t)P * nv); row_off.ensure((size_t)P * nv); gmax.ensure(4);
+        u.ensure(np); dt.ensure(np); c1d.ensure(np); pbat.ensure(np); act.ensure(np);
     }
     PairGeom<Real> view() {
         return PairGeom<Real>{count.p, row_off.p, u.p, dt.p, c1d.p, pbat.p, act.p, row.p, gmax.p};
@@ -283,10 +309,12 @@ int light_first(const Geometry<Real>& G, int nt, int nlaunch);
 // Compacted pair records + SoC row records for P plans (dims filled by the
 // caller).  The row buffer is sized from the feasible-pair count (kept across
 // rebuilds of the same route, so refits allocate nothing).
+// with_tiles = false: pair + SoC-row records only (what the terminal-field
+// sweep reads), no stage-kernel tile plans.
 template <typename Real>
 void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d_plans, const double* d_vaxes,
                     const double* d_te, const double* d_tb, const double* d_soc, const EcoStage1Tables& d_tab,
-                    cudaStream_t st, int64_t* launches) {
+                    cudaStream_t st, int64_t* launches, bool with_tiles = true) {
     const GeomDims& g = G.dims;
     if (G.act.n != (size_t)g.P * g.nv * g.U) G.alloc(g.P, g.nv, g.U);
     ECO_CUDA(cudaMemsetAsync(G.gmax.p, 0, 4 * sizeof(int32_t), st));
@@ -303,7 +331,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     ECO_CUDA(cudaMemcpyAsync(G.h_gmax, G.gmax.p, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     ECO_CUDA(cudaStreamSynchronize(st));
     G.rows_total = last_off + (int64_t)last_cnt * g.nx;
-    if (G.row.n < (size_t)std::max<int64_t>(1, G.rows_total)) G.row.alloc((size_t)std::max<int64_t>(1, G.rows_total));
+    if (G.row.cap < (size_t)std::max<int64_t>(1, G.rows_total)) G.row.alloc((size_t)std::max<int64_t>(1, G.rows_total));
     const size_t smem = (size_t)g.ntb * g.nx * (sizeof(double) + 1) + 16;
     if (smem > 48 * 1024)
         ECO_CUDA(cudaFuncSetAttribute(geom_soc_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -312,16 +340,25 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     ECO_CUDA(cudaGetLastError());
     geom_unpack_u_kernel<<<npi, 256, 0, st>>>(G.u.p, G.count.p, g.U);
     ECO_CUDA(cudaGetLastError());
+    if (!with_tiles) {
+        if (launches) *launches += 4;
+        return;
+    }
     // staging plans of the (v, soc, t) stage kernel's tiles
     const int upr = (g.nt + kZP - 1) / kZP;
     const int tj_default = G.tj_pref > 0 ? G.tj_pref : (wide_rows(g.nt) ? 2 : std::max(1, 16 / upr));
     G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", tj_default)));
     G.nchunk = (g.nx + G.tj - 1) / G.tj;
-    G.band_cap = env_int("ECO_BAND_KB", 40) * 1024 / (int)sizeof(Real);
+    // wide-row tiles never stage a band (and get no RowRec2 buffer): cap -1
+    // marks every one of them unstaged
+    G.band_cap = wide_rows(g.nt) ? -1 : env_int("ECO_BAND_KB", 40) * 1024 / (int)sizeof(Real);
     const size_t ntiles = (size_t)npi * G.nchunk;
-    if (G.tiles.n != ntiles) G.tiles.alloc(ntiles);
-    if (G.row2.n < G.row.n) G.row2.alloc(G.row.n);
-    if (G.order.n != ntiles) { G.order.alloc(ntiles); G.rank_of.alloc(ntiles); }
+    G.tiles.ensure(ntiles);
+    // RowRec2 (shared-memory band bases) only serve the staged narrow path:
+    // wide-row tiles never stage a band
+    if (!wide_rows(g.nt) && G.row2.cap < G.row.cap) G.row2.alloc(G.row.cap);
+    G.order.ensure(ntiles);
+    G.rank_of.ensure(ntiles);
     const int phi = G.phi < 0 ? g.nv : G.phi;
     const int chunk_major = env_int("ECO_CHUNK_MAJOR", wide_rows(g.nt) ? 1 : 0);
     const int light = chunk_major ? 0 : light_first<Real>(G, g.nt, (phi - G.plo) * G.nchunk);
@@ -641,7 +678,7 @@ struct HorizonInputs {
         std::memcpy(h + o_te, pr->te_axis, sizeof(double) * pr->n_te);
         std::memcpy(h + o_tb, pr->tb_axis, sizeof(double) * pr->n_tb);
         std::memcpy(h + o_soc, pr->soc_axis, sizeof(double) * nx);
-        if (term) std::memcpy(h + o_term, term, sizeof(double) * ns);
+        if (term) parallel_memcpy(h + o_term, term, sizeof(double) * ns);
         ECO_CUDA(cudaMemcpyAsync(blob.p, host, off, cudaMemcpyHostToDevice, st));
         char* d = blob.p;
         plant = reinterpret_cast<EcoPlant*>(d + o_plant);
@@ -704,7 +741,10 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     cudaStream_t st = 0;
     int64_t launches = 0;
     HorizonInputs& in = horizon_inputs();
+    const bool dbg_io = env_int("ECO_DEBUG_IO", 0) != 0;
+    const auto h0 = std::chrono::steady_clock::now();
     in.upload(plant, pr, plans, H, terminal, st);
+    const auto h1 = std::chrono::steady_clock::now();
     TablesDev tdev;   // plant path: no tables
 
     // device buffers persist across calls (grow-only workspace): repeated
@@ -811,6 +851,10 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         // level k is final once stage k ran: its conversion and download run
         // on a side stream while the remaining stages sweep
         all.stop(st);
+        // pinned destinations: every level's conversion + DMA is enqueued at
+        // once (the copy engine streams levels out as the sweep produces
+        // them); pageable ones go through download_big's staging per level
+        const bool direct = host_pinned(J_stack) && host_pinned(P_stack);
         for (int k = H; k >= 0; --k) {
             ECO_CUDA(cudaStreamWaitEvent(ovs, lvl_ev[k], 0));
             to_external_levels_kernel<Real><<<grid_for(ns), 256, 0, ovs>>>(d_J.p + (size_t)k * LV,
@@ -818,8 +862,24 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
                                                                            pr->j_inf);
             ECO_CUDA(cudaGetLastError());
             ++launches;
+            if (direct) {
+                ECO_CUDA(cudaMemcpyAsync(J_stack + (size_t)k * ns, d_tmp.p + (size_t)k * ns, ns * sizeof(double),
+                                         cudaMemcpyDeviceToHost, ovs));
+                if (k < H)
+                    ECO_CUDA(cudaMemcpyAsync(P_stack + (size_t)k * ns, d_P.p + (size_t)k * ns, ns * sizeof(int32_t),
+                                             cudaMemcpyDeviceToHost, ovs));
+                continue;
+            }
             download_big(J_stack + (size_t)k * ns, d_tmp.p + (size_t)k * ns, ns * sizeof(double), ovs);
             if (k < H) download_big(P_stack + (size_t)k * ns, d_P.p + (size_t)k * ns, ns * sizeof(int32_t), ovs);
+        }
+        if (direct) ECO_CUDA(cudaStreamSynchronize(ovs));
+        if (dbg_io) {
+            const auto h2 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "io: upload(host) %.2f ms, all %.2f ms, direct=%d, outputs done at %.2f ms after "
+                                 "the upload\n",
+                         std::chrono::duration<double, std::milli>(h1 - h0).count(), all.ms(), direct ? 1 : 0,
+                         std::chrono::duration<double, std::milli>(h2 - h1).count());
         }
     } else {
         to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, H + 1,
@@ -945,10 +1005,15 @@ struct FieldGraph {
     }
 };
 
+// chunk (nullable): geometry on demand -- chunk(m0, m1) builds plans
+// [m0, m1) into G (plan m at index m - m0) for grids whose all-route
+// geometry does not fit; the sweep then walks the route backwards chunk by
+// chunk, chunk_plans plans at a time (no graph: the builds sync the host).
 template <typename Real>
 void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConfig* c, Geometry<Real>& G,
                       RouteDev& R, const double* d_soc, DBuf<Real>& d_G, DBuf<double>& d_field_ext,
-                      cudaStream_t st, int64_t* launches, double* sweep_ms, FieldGraph* fg = nullptr) {
+                      cudaStream_t st, int64_t* launches, double* sweep_ms, FieldGraph* fg = nullptr,
+                      const std::function<void(int, int)>& chunk = {}, int chunk_plans = 0) {
     const int nv = c->n_v, nx = c->n_soc;
     const size_t lvl = (size_t)nv * nx;
     field_init_kernel<<<1, 256, 0, st>>>(d_soc, R.vaxes.p + (size_t)(n - 1) * nv, nv, nx, c->soc_target,
@@ -958,10 +1023,11 @@ void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConf
                                                             d_G.p + (size_t)(n - 1) * lvl, lvl, c->j_inf);
     ECO_CUDA(cudaGetLastError());
     *launches += 2;
-    const TileCfg tc = tile_cfg(G, 1, 1);
-    auto enqueue = [&](cudaStream_t qs) {
-        for (int s = n - 2; s >= 0; --s) {
-            StageArgs<Real> a = stage_args(G, s, R.vaxes.p + (size_t)s * nv, 1, tc);
+    // stages s = s_hi - 1 .. s_lo of the sweep; plan s sits at index s - base of G
+    auto enqueue = [&](cudaStream_t qs, int s_lo, int s_hi, int base) {
+        const TileCfg tc = tile_cfg(G, 1, 1);
+        for (int s = s_hi - 1; s >= s_lo; --s) {
+            StageArgs<Real> a = stage_args(G, s - base, R.vaxes.p + (size_t)s * nv, 1, tc);
             a.J_next = d_G.p + (size_t)(s + 1) * lvl;
             a.J_out = d_G.p + (size_t)s * lvl;
             a.P_out = nullptr;
@@ -972,35 +1038,52 @@ void field_build_impl(const int8_t* kinds, int n, double dwell, const EcoMpcConf
             launch_stage<Real, 1>(a, tc, false, qs);
         }
     };
-    EventTimer tm;
-    if (fg && st && env_int("ECO_GRAPH", 1) != 0) {
+    double ms = 0.0;
+    if (chunk) {
+        const int C = std::max(1, chunk_plans);
+        for (int m1 = n - 1; m1 > 0;) {
+            const int m0 = std::max(0, m1 - C);
+            chunk(m0, m1);
+            EventTimer tm;
+            tm.start(st);
+            enqueue(st, m0, m1, m0);
+            tm.stop(st);
+            ms += tm.ms();
+            m1 = m0;
+        }
+    } else if (fg && st && env_int("ECO_GRAPH", 1) != 0) {
         // the N-1 launches as one graph (captured once per geometry / buffers)
+        const TileCfg tc = tile_cfg(G, 1, 1);
         const std::vector<long long> key = {(long long)(size_t)G.act.p, (long long)(size_t)G.row.p,
                                             (long long)(size_t)d_G.p, tc.slices, n};
         if (!fg->exec || fg->key != key) {
             if (fg->exec) { cudaGraphExecDestroy(fg->exec); fg->exec = nullptr; }
             cudaGraph_t graph;
             ECO_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            enqueue(st);
+            enqueue(st, 0, n - 1, 0);
             ECO_CUDA(cudaStreamEndCapture(st, &graph));
             ECO_CUDA(cudaGraphInstantiate(&fg->exec, graph, 0));
             cudaGraphDestroy(graph);
             fg->key = key;
         }
+        EventTimer tm;
         tm.start(st);
         ECO_CUDA(cudaGraphLaunch(fg->exec, st));
         tm.stop(st);
+        ms = tm.ms();
     } else {
+        EventTimer tm;
         tm.start(st);
-        enqueue(st);
+        enqueue(st, 0, n - 1, 0);
         tm.stop(st);
+        ms = tm.ms();
     }
     *launches += n - 1;
     to_external_kernel<Real><<<grid_for((size_t)(n - 1) * lvl), 256, 0, st>>>(d_G.p, d_field_ext.p,
                                                                              (size_t)(n - 1) * lvl, c->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++*launches;
-    if (sweep_ms) *sweep_ms += tm.ms();
+    if (sweep_ms) *sweep_ms += ms;
 }
 
 void check_cfg(const EcoMpcConfig* c) {
@@ -1032,7 +1115,8 @@ struct RouteCtx {
     std::vector<double> h_soc;
     Geometry<Real> G;
 
-    void init(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, cudaStream_t st) {
+    // ring: no all-route geometry (fine grids build plans on demand)
+    void init(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c, cudaStream_t st, bool ring = false) {
         plant.alloc(1);
         plant.upload(p, 1, st);
         R.upload(r, c->n_v, st);
@@ -1047,7 +1131,7 @@ struct RouteCtx {
         soc.upload(h_soc.data(), c->n_soc, st);
         G.dims = GeomDims{r->node_count - 1, c->n_v, c->n_soc, c->n_t, c->n_te * c->n_tb, c->n_te, c->n_tb,
                           r->delta_d, r->accel_min, r->accel_max, c->gamma, c->dt};
-        G.alloc(G.dims.P, G.dims.nv, G.dims.U);
+        if (!ring) G.alloc(G.dims.P, G.dims.nv, G.dims.U);
     }
     // new route data of the same shape (speed limits, grades, node kinds,
     // signal programs): arrays re-uploaded in place, plans rebuilt
@@ -1115,6 +1199,31 @@ struct Session : SessionBase {
     cudaGraphExec_t gexec = nullptr;
     std::vector<long long> gkey;
     FieldGraph fgraph;             // the terminal-field sweep, replayed per fit
+    // Ring mode (grids whose all-route geometry does not fit in HBM, e.g. the
+    // C3 grid: ~0.3 GB of records per plan, 699 plans): the H + 1 plans a
+    // receding-horizon step can touch live in a ring of slots; plan s + H is
+    // built on a side stream while step s sweeps, into the slot plan s - 1
+    // vacated.  The terminal field is swept chunk by chunk.
+    bool ring = false;
+    std::vector<std::unique_ptr<Geometry<Real>>> slots;
+    std::vector<int> slot_plan;
+    std::vector<cudaEvent_t> slot_ev;
+    Geometry<Real> fieldG;
+    int field_chunk = 1;
+    cudaStream_t geo_st = nullptr;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    int32_t* h_status = nullptr;   // pinned mirror of the loop status, per step parity
+
+    static bool decide_ring(const EcoMpcConfig* c, int n) {
+        const int forced = env_int("ECO_RING", -1);
+        if (forced >= 0) return forced != 0;
+        const double U = (double)c->n_te * c->n_tb;
+        // records of all plans at ~35 % feasible (plan, plane, action, SoC row)
+        const double est = (double)(n - 1) * c->n_v * U * (44.0 + 0.35 * c->n_soc * 32.0);
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return est > 40e9;
+        return est > 0.3 * (double)fr;
+    }
 
     Session(const EcoPlant* p, const EcoRoute* r, const EcoMpcConfig* c) {
         cfg = *c;
@@ -1125,7 +1234,21 @@ struct Session : SessionBase {
         n = r->node_count;
         kinds.assign(r->kinds, r->kinds + n);
         stop_dwell = r->stop_dwell;
-        ctx.init(p, r, &cfg, st);
+        ring = decide_ring(c, n);
+        ctx.init(p, r, &cfg, st, ring);
+        if (ring) {
+            const int H1 = c->horizon + 1;
+            slots.resize(H1);
+            for (auto& g : slots) g = std::make_unique<Geometry<Real>>();
+            slot_plan.assign(H1, -1);
+            slot_ev.resize(H1);
+            for (auto& e : slot_ev) ECO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (auto& e : stage_ev) ECO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ECO_CUDA(cudaStreamCreateWithFlags(&geo_st, cudaStreamNonBlocking));
+            ECO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_status), 2 * sizeof(int32_t), cudaHostAllocDefault));
+            const double per_plan = (double)c->n_v * c->n_te * c->n_tb * (44.0 + 0.35 * c->n_soc * 16.0);
+            field_chunk = (int)std::max(1.0, std::min((double)(n - 1), 8e9 / per_plan));
+        }
         const int nv = cfg.n_v, nx = cfg.n_soc, nt = cfg.n_t, H = cfg.horizon;
         const size_t ns = (size_t)nv * nx * nt;
         field.alloc((size_t)n * nv * nx);
@@ -1143,6 +1266,10 @@ struct Session : SessionBase {
         ECO_CUDA(cudaStreamCreate(&st));
     }
     ~Session() override {
+        for (auto& e : slot_ev) if (e) cudaEventDestroy(e);
+        for (auto& e : stage_ev) if (e) cudaEventDestroy(e);
+        if (geo_st) cudaStreamDestroy(geo_st);
+        if (h_status) cudaFreeHost(h_status);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (dec_fork) cudaEventDestroy(dec_fork);
         if (dec_join) cudaEventDestroy(dec_join);
@@ -1178,15 +1305,30 @@ struct Session : SessionBase {
         fitted = false;              // geometry and field depend on the route
     }
 
+    // plans [m0, m1) into G (P = m1 - m0), from the uploaded route
+    void build_plans(Geometry<Real>& G, int m0, int m1, cudaStream_t qs, int64_t* launches, bool tiles) {
+        G.dims = ctx.G.dims;
+        G.dims.P = m1 - m0;
+        EcoStage1Tables none{};
+        build_geometry(G, ctx.plant.p, ctx.plans.p + m0, ctx.R.vaxes.p + (size_t)m0 * cfg.n_v, ctx.te.p, ctx.tb.p,
+                       ctx.soc.p, none, qs, launches, tiles);
+    }
+
     void fit(const double* field_in, double* field_out, EcoStats* stats) override {
         int64_t launches = 0;
         EventTimer all;
         all.start(st);
-        ctx.geometry(st, &launches);
+        if (!ring) ctx.geometry(st, &launches);
+        else std::fill(slot_plan.begin(), slot_plan.end(), -1);     // the route may have changed
         double sweep_ms = 0.0;
         const size_t lvl = (size_t)cfg.n_v * cfg.n_soc;
         if (cfg.use_terminal_field) {
             if (field_in) field.upload(field_in, (size_t)n * lvl, st);
+            else if (ring)
+                field_build_impl<Real>(kinds.data(), n, stop_dwell, &cfg, fieldG, ctx.R, ctx.soc.p, field_int, field,
+                                       st, &launches, &sweep_ms, nullptr,
+                                       [&](int m0, int m1) { build_plans(fieldG, m0, m1, st, &launches, false); },
+                                       field_chunk);
             else field_build_impl<Real>(kinds.data(), n, stop_dwell, &cfg, ctx.G, ctx.R, ctx.soc.p, field_int,
                                         field, st, &launches, &sweep_ms, &fgraph);
         }
@@ -1221,7 +1363,7 @@ struct Session : SessionBase {
         LoopCfg lc{nv, nx, nt, cfg.n_te, cfg.n_tb, U, H, cfg.teleport, cfg.use_terminal_field, cfg.dt, cfg.gamma,
                    cfg.soc_target, cfg.soc_weight, cfg.j_inf, ctx.te.p, ctx.tb.p, ctx.soc.p, ctx.R.vaxes.p};
         const int s_end = max_steps < 0 ? n - 1 : std::min(n - 1, start_node + max_steps);
-        const TileCfg tc = tile_cfg(ctx.G, nt, 0);
+        const TileCfg tc = ring ? TileCfg{} : tile_cfg(ctx.G, nt, 0);
         if (!dec_side) {
             ECO_CUDA(cudaStreamCreateWithFlags(&dec_side, cudaStreamNonBlocking));
             ECO_CUDA(cudaEventCreateWithFlags(&dec_fork, cudaEventDisableTiming));
@@ -1302,8 +1444,110 @@ struct Session : SessionBase {
                 ++launches;
             }
         };
-        const bool use_graph = !count && env_int("ECO_GRAPH", 1) != 0;
-        if (use_graph) {
+        // ring mode: the same per-step sequence, launched directly (plan
+        // builds sync the host: no graph), the geometry of the step's new
+        // plan built beside the previous step's sweeps
+        auto ring_enqueue = [&]() {
+            stages = 0;
+            launches = 0;
+            const size_t LV = level_stride(ns), LC = level_copy(ns);
+            const int seed_grid = std::max(1, (int)std::min<size_t>(148, (ns + 255) / 256));
+            const double* fld = cfg.use_terminal_field ? (const double*)field.p : nullptr;
+            auto Jstack = [&](int s) { return J.p + (size_t)((s - start_node) & 1) * (H + 1) * LV; };
+            auto horizon = [&](int s) { return H < n - 1 - s ? H : n - 1 - s; };
+            const int H1 = H + 1;
+            auto ensure_plan = [&](int m, cudaStream_t qs) {
+                const int j = m % H1;
+                if (slot_plan[j] == m) return;
+                slot_plan[j] = -1;
+                build_plans(*slots[j], m, m + 1, qs, &launches, true);
+                slot_plan[j] = m;
+                ECO_CUDA(cudaEventRecord(slot_ev[j], qs));
+            };
+            ECO_CUDA(cudaStreamSynchronize(geo_st));     // a previous run's last plan build
+            for (int m = start_node; m < start_node + horizon(start_node); ++m) ensure_plan(m, st);
+            h_status[0] = h_status[1] = 0;
+            for (int s = start_node; s < s_end; ++s) {
+                // the device loop stopped (infeasible / plant failure): the
+                // status of step s - 2 has reached the host by now
+                if (s - start_node >= 2 && h_status[s & 1] != 0) break;
+                const int h = horizon(s);
+                Real* Js = Jstack(s);
+                if (s == start_node) {
+                    mpc_ladders_kernel<<<1, 256, 0, st>>>(ctx.R.view, lc, state.p, s, h, lad);
+                    mpc_seed_kernel<Real><<<seed_grid, 256, 0, st>>>(lc, s, h, fld, Js + (size_t)h * LV,
+                                                                     Js + (size_t)h * LV + LC);
+                    ECO_CUDA(cudaGetLastError());
+                    launches += 2;
+                }
+                ECO_CUDA(cudaEventRecord(dec_fork, st));
+                ECO_CUDA(cudaStreamWaitEvent(dec_side, dec_fork, 0));
+                mpc_candidates_kernel<<<(U + kCandThreads - 1) / kCandThreads, kCandThreads, 0, dec_side>>>(
+                    ctx.plant.p, ctx.R.view, lc, state.p, s, lad, dec_cand.p, dec_head.p);
+                ++launches;
+                if (s + 1 < s_end) {
+                    const int h1 = horizon(s + 1);
+                    Real* Jn = Jstack(s + 1);
+                    mpc_seed_kernel<Real><<<seed_grid, 256, 0, dec_side>>>(lc, s + 1, h1, fld, Jn + (size_t)h1 * LV,
+                                                                          Jn + (size_t)h1 * LV + LC);
+                    ++launches;
+                }
+                ECO_CUDA(cudaGetLastError());
+                ECO_CUDA(cudaEventRecord(dec_join, dec_side));
+                for (int m = s; m < s + h; ++m) ECO_CUDA(cudaStreamWaitEvent(st, slot_ev[m % H1], 0));
+                for (int k = h - 1; k >= 0; --k) {
+                    Geometry<Real>& G = *slots[(s + k) % H1];
+                    const TileCfg tk = tile_cfg(G, nt, 0);
+                    StageArgs<Real> a = stage_args(G, 0, ctx.R.vaxes.p + (size_t)(s + k) * nv, nt, tk);
+                    a.green = green.p + (size_t)(k + 1) * nt;
+                    a.dep_ok = dep.p + (size_t)k * nt;
+                    a.t_dep = tdep.p + (size_t)k * nt;
+                    a.wait = wait.p + (size_t)k * nt;
+                    a.J_next = Js + (size_t)(k + 1) * LV;
+                    a.J_next1 = a.J_next + LC;
+                    a.J_out = Js + (size_t)k * LV;
+                    a.J_out1 = G.all_staged ? nullptr : a.J_out + LC;
+                    a.P_out = nullptr;
+                    a.status = &state.p->status;
+                    a.live = count ? live.p : nullptr;
+                    a.src_kind = kinds[s + k];
+                    a.flags = sflags.p + k;
+                    a.t0_dev = tax.p;
+                    a.dtg = cfg.dt;
+                    a.j_inf = (Real)cfg.j_inf;
+                    launch_stage<Real, 0>(a, tk, count, st);
+                    ++launches;
+                    ++stages;
+                }
+                ECO_CUDA(cudaEventRecord(stage_ev[s & 1], st));
+                ECO_CUDA(cudaStreamWaitEvent(st, dec_join, 0));
+                const int s_next = s + 1 < s_end ? s + 1 : -1;
+                launch_pdl(mpc_pick_kernel<Real>, 1, std::min(kDecideThreads, (U + 31) / 32 * 32), st, true,
+                           (const EcoPlant*)ctx.plant.p, ctx.R.view, lc, state.p, s, h, (const Real*)(Js + LV),
+                           (const DecideCand*)dec_cand.p, (const DecideHead*)dec_head.p, lad, rows.p, step_ns.p,
+                           s_next, s_next < 0 ? 0 : horizon(s_next));
+                ECO_CUDA(cudaGetLastError());
+                ++launches;
+                ECO_CUDA(cudaMemcpyAsync(h_status + (s & 1), &state.p->status, sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, st));
+                // the plan step s + 1 adds, built while step s sweeps, into the
+                // slot plan s - 1 held (free once step s - 1's sweeps are done)
+                if (s + 1 < s_end) {
+                    const int m = s + horizon(s + 1);
+                    if (slot_plan[m % H1] != m) {
+                        ECO_CUDA(cudaStreamWaitEvent(geo_st, stage_ev[(s - 1) & 1], 0));
+                        ensure_plan(m, geo_st);
+                    }
+                }
+            }
+        };
+        const bool use_graph = !ring && !count && env_int("ECO_GRAPH", 1) != 0;
+        if (ring) {
+            all.start(st);
+            state.upload(&h0, 1, st);
+            if (count) ECO_CUDA(cudaMemsetAsync(live.p, 0, sizeof(unsigned long long), st));
+            ring_enqueue();
+        } else if (use_graph) {
             const std::vector<long long> key = {start_node, s_end, (long long)(size_t)ctx.G.row2.p,
                                                 (long long)(size_t)ctx.G.tiles.p, (long long)(size_t)ctx.G.order.p,
                                                 (long long)(size_t)field.p, tc.tj, tc.slices,
@@ -1333,6 +1577,7 @@ struct Session : SessionBase {
             enqueue(st);
         }
         all.stop(st);
+        if (ring) ECO_CUDA(cudaStreamSynchronize(geo_st));
         LoopState hs{};
         state.download(&hs, 1, st);
         unsigned long long nlive = 0;
@@ -1720,6 +1965,9 @@ struct Slab : SlabBase {
         connected = true;
     }
 
+    // After stage k: every rank holds copy 0 of the full level (peers' slabs
+    // arrived by NVLink stores + barrier, or by broadcast); copy 1 (the
+    // shifted twin) is rebuilt locally instead of crossing the links.
     void exchange_level(int k) {
         Real* Lk = J.p + (size_t)k * LV;
         const size_t plane = (size_t)nx * nt;
@@ -1728,20 +1976,19 @@ struct Slab : SlabBase {
             slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
                                                   (unsigned)(barriers * nranks), err.p);
             ECO_CUDA(cudaGetLastError());
-            return;
+        } else {
+            const ncclDataType_t ty = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
+            if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+            for (int g = 0; g < nranks; ++g) {
+                const size_t o0 = (size_t)lo[g] * plane, n0 = (size_t)(hi[g] - lo[g]) * plane;
+                if (!n0) continue;
+                if (ncclBroadcast(Lk + o0, Lk + o0, n0, ty, g, comm, st) != ncclSuccess)
+                    throw std::runtime_error("ncclBroadcast failed");
+            }
+            if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
         }
-        const ncclDataType_t ty = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
-        if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
-        for (int g = 0; g < nranks; ++g) {
-            const size_t o0 = (size_t)lo[g] * plane, n0 = (size_t)(hi[g] - lo[g]) * plane;
-            if (!n0) continue;
-            // copy 0 and its shifted twin (copy 1 holds J[i + 1] at i)
-            const size_t a1 = o0 ? o0 - 1 : 0, b1 = o0 + n0 - 1;
-            if (ncclBroadcast(Lk + o0, Lk + o0, n0, ty, g, comm, st) != ncclSuccess ||
-                ncclBroadcast(Lk + LC + a1, Lk + LC + a1, b1 - a1, ty, g, comm, st) != ncclSuccess)
-                throw std::runtime_error("ncclBroadcast failed");
-        }
-        if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
+        shift_copy_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(Lk, ns, LC);
+        ECO_CUDA(cudaGetLastError());
     }
 
     void solve(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H, const double* terminal,
@@ -1806,7 +2053,7 @@ struct Slab : SlabBase {
             ++launches;
             if (nranks > 1) {
                 exchange_level(k);
-                ++launches;
+                launches += 2;
             }
         }
         sweep.stop(st);
@@ -1836,6 +2083,96 @@ struct Slab : SlabBase {
     }
 };
 
+// eco_slab_emulate: nranks slab ranks on ONE GPU (kernel-boundary stage
+// barrier, one launch per stage over every rank's tiles); every rank keeps its
+// own replica of the levels, filled by its own stores and its peers' PEERS
+// epilogue stores (copy 0) + the local copy-1 rebuild, as on a multi-GPU run.
+template <typename Real>
+void slab_emulate_impl(int nranks, const int32_t* bounds, const EcoPlant* plant, const EcoProblem* pr,
+                       const EcoStepPlan* plans, int H, const double* terminal, double* J_stacks, int32_t* P_stack,
+                       EcoStats* stats) {
+    const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t, U = pr->n_te * pr->n_tb;
+    if (nranks < 1 || nranks > kEmulMaxRanks) throw ArgError{"emulation supports 1..8 ranks"};
+    if (bounds[0] != 0 || bounds[nranks] != nv) throw ArgError{"partition does not cover the speed planes"};
+    for (int g = 0; g < nranks; ++g)
+        if (bounds[g + 1] <= bounds[g]) throw ArgError{"partition ranges must be non-empty and ordered"};
+    const size_t ns = (size_t)nv * nx * nt, LV = level_stride(ns), LC = level_copy(ns);
+    cudaStream_t st = 0;
+    int64_t launches = 0;
+    HorizonInputs in;
+    in.upload(plant, pr, plans, H, terminal, st);
+    Geometry<Real> G;
+    G.dims = GeomDims{H, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
+    TablesDev tdev;
+    build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+    DBuf<Real> rep((size_t)nranks * (H + 1) * LV);
+    DBuf<int32_t> P((size_t)H * ns);
+    EmulArgs<Real> e{};
+    std::vector<Real*> peers;
+    for (int g = 0; g < nranks; ++g) {
+        e.rep[g] = rep.p + (size_t)g * (H + 1) * LV;
+        e.lo[g] = bounds[g];
+        for (int q = 0; q < nranks; ++q)
+            if (q != g) peers.push_back(rep.p + (size_t)q * (H + 1) * LV);
+        to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(in.terminal, e.rep[g] + (size_t)H * LV, ns,
+                                                                     pr->j_inf);
+        ECO_CUDA(cudaGetLastError());
+    }
+    e.lo[nranks] = nv;
+    e.nranks = nranks;
+    e.lc = LC;
+    DBuf<Real*> d_peers(std::max<size_t>(1, peers.size()));
+    if (!peers.empty()) d_peers.upload(peers.data(), peers.size(), st);
+    e.peers = d_peers.p;
+    const TileCfg tc = tile_cfg(G, nt, 0);
+    auto kern = tc.wide ? bellman_emul_kernel<Real, true> : bellman_emul_kernel<Real, false>;
+    set_smem_attr(kern, tc.smem);
+    EventTimer all;
+    all.start(st);
+    for (int k = H - 1; k >= 0; --k) {
+        StageArgs<Real> a = stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
+        a.green = in.green + (size_t)k * nt;
+        a.flags = in.flags + k;
+        a.dep_ok = in.dep + (size_t)k * nt;
+        a.t_dep = in.tdep + (size_t)k * nt;
+        a.wait = in.wait + (size_t)k * nt;
+        a.P_out = P.p + (size_t)k * ns;
+        a.src_kind = plans[k].src_kind;
+        a.t0 = pr->t0;
+        a.dtg = pr->dtg;
+        a.j_inf = (Real)pr->j_inf;
+        a.lc = LC;
+        e.next_off = (size_t)(k + 1) * LV;
+        e.out_off = (size_t)k * LV;
+        kern<<<nv * tc.nchunk, tc.S * tc.slices, tc.smem, st>>>(a, e);
+        ECO_CUDA(cudaGetLastError());
+        ++launches;
+        for (int g = 0; g < nranks; ++g) {
+            shift_copy_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(e.rep[g] + (size_t)k * LV, ns, LC);
+            ECO_CUDA(cudaGetLastError());
+            ++launches;
+        }
+    }
+    all.stop(st);
+    DBuf<double> tmp(ns * (H + 1));
+    for (int g = 0; g < nranks; ++g) {
+        to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(e.rep[g], tmp.p, ns, H + 1,
+                                                                               pr->j_inf);
+        ECO_CUDA(cudaGetLastError());
+        download_big(J_stacks + (size_t)g * (H + 1) * ns, tmp.p, ns * (H + 1) * sizeof(double), st);
+    }
+    if (P_stack) download_big(P_stack, P.p, (size_t)H * ns * sizeof(int32_t), st);
+    ECO_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+        stats->device_ms = all.ms();
+        stats->dominant_ms = stats->device_ms;
+        stats->dense_updates = (int64_t)ns * U * H;
+        stats->live_updates = -1;
+        stats->stages = H;
+        stats->kernel_launches = launches;
+    }
+}
+
 SlabBase* make_slab(int nranks, int rank, int exchange, const int32_t* bounds, int precision, int nv, int nx, int nt,
                     int Hmax) {
     SlabBase* s;
@@ -1859,6 +2196,20 @@ int32_t eco_release_workspace(void) {
         std::lock_guard<std::mutex> lock(workspace_mutex());
         horizon_workspace<float>().release();
         horizon_workspace<double>().release();
+    });
+}
+
+int32_t eco_host_alloc(uint64_t bytes, void** out) {
+    return run_guarded([&] {
+        if (!out) throw ArgError{"null pointer argument"};
+        *out = nullptr;
+        if (bytes) ECO_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+    });
+}
+
+int32_t eco_host_free(void* p) {
+    return run_guarded([&] {
+        if (p) ECO_CUDA(cudaFreeHost(p));
     });
 }
 
@@ -2072,6 +2423,20 @@ int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant, const EcoProblem* p
         if (!slab || !plans || !terminal) throw ArgError{"null pointer argument"};
         reinterpret_cast<SlabBase*>(slab)->solve(plant, prob, plans, H, terminal, J_stack, P_slab, count_live,
                                                  stats);
+    });
+}
+
+int32_t eco_slab_emulate(int32_t nranks, const int32_t* bounds, int32_t precision, const EcoPlant* plant,
+                         const EcoProblem* prob, const EcoStepPlan* plans, int32_t H, const double* terminal,
+                         double* J_stacks, int32_t* P_stack, EcoStats* stats) {
+    return run_guarded([&] {
+        check_plant(plant);
+        check_problem(prob);
+        if (!bounds || !plans || !terminal || !J_stacks || H < 1) throw ArgError{"bad arguments"};
+        if (precision == ECO_FP64)
+            slab_emulate_impl<double>(nranks, bounds, plant, prob, plans, H, terminal, J_stacks, P_stack, stats);
+        else
+            slab_emulate_impl<float>(nranks, bounds, plant, prob, plans, H, terminal, J_stacks, P_stack, stats);
     });
 }
 

@@ -686,14 +686,22 @@ struct TileSmem {
 // 64-bit load.  Standstill planes (v == 0: red-wait / dwell relocation,
 // K:519-535) run a per-state loop.
 // C5 P2P exchange: the slab's outputs go straight into every peer's replica
-// of the level (NVLink stores), both copies.
+// of the level (NVLink stores), copy 0 only -- each rank rebuilds its shifted
+// copy 1 locally once the stage barrier has passed (shift_copy_kernel), so
+// the links carry each element once.
 template <typename Real>
 __device__ __forceinline__ void store_peers(const StageArgs<Real>& a, size_t i, Real val) {
-    for (int g = 0; g < a.npeer; ++g) {
-        Real* pb = a.peer_base[g] + a.peer_off;
-        pb[i] = val;
-        if (i > 0) pb[a.lc + i - 1] = val;
-    }
+    for (int g = 0; g < a.npeer; ++g) a.peer_base[g][a.peer_off + i] = val;
+}
+
+// copy 1 of a level from its copy 0 (copy1[i] = copy0[i + 1], +inf past the
+// end): the local half of the slab exchange
+template <typename Real>
+__global__ void shift_copy_kernel(Real* __restrict__ level, size_t n, size_t lc) {
+    const Real* c0 = level;
+    Real* c1 = level + lc;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n + 8; i += (size_t)gridDim.x * blockDim.x)
+        c1[i] = i + 1 < n ? c0[i + 1] : (Real)INFINITY;
 }
 
 // Candidate acceptance of one thread's action scan (ascending flat index):
@@ -1335,6 +1343,41 @@ bellman_wide_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem[];
     stage_tile<Real, COUNT, true, PEERS, false, REV>(a, blockIdx.x, smem);
+}
+
+// Single-GPU emulation of a G-rank slab stage (tests of the C5 exchange on a
+// one-GPU lease, where ranks whose kernels wait on one another cannot run as
+// separate launches): ONE launch covers every rank's tiles; a CTA of a tile
+// on plane iv acts as the rank owning iv -- it reads J_{k+1} from that rank's
+// replica, writes its outputs there and stores them into every other
+// replica through the same PEERS epilogue the multi-GPU kernel uses.  The
+// kernel boundary is the stage barrier.
+constexpr int kEmulMaxRanks = 8;
+template <typename Real>
+struct EmulArgs {
+    Real* rep[kEmulMaxRanks];      // level-0 base of each rank's replica
+    int lo[kEmulMaxRanks + 1];     // plane bounds
+    Real* const* peers;            // [G][G-1] peer bases per owning rank
+    size_t next_off, out_off, lc;
+    int nranks;
+};
+
+template <typename Real, bool WIDE>
+__global__ void __launch_bounds__(256, WIDE ? ECO_WIDE_MINB : ECO_STAGE_MINB)
+bellman_emul_kernel(StageArgs<Real> a, EmulArgs<Real> e) {
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int iv = a.tiles[blockIdx.x].iv;
+    int g = 0;
+    while (g + 1 < e.nranks && iv >= e.lo[g + 1]) ++g;
+    a.J_next = e.rep[g] + e.next_off;
+    a.J_next1 = a.J_next + e.lc;
+    a.J_out = e.rep[g] + e.out_off;
+    a.J_out1 = a.J_out + e.lc;
+    a.peer_base = e.peers + (size_t)g * (e.nranks - 1);
+    a.npeer = e.nranks - 1;
+    a.peer_off = e.out_off;
+    stage_tile<Real, false, WIDE, true, !WIDE>(a, blockIdx.x, smem);
 }
 
 // Batch of independent solves sharing one route's geometry (run_bench's

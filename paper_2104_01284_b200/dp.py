@@ -389,8 +389,10 @@ class SolveResult:
 
 
 def release_workspace():
-    """Free the device workspace the stateless solvers keep between calls."""
+    """Free the device workspace the stateless solvers keep between calls
+    and the idle page-locked output blocks."""
     _abi.check(_abi.lib().eco_release_workspace(), "eco_release_workspace")
+    _abi.PINNED.clear()
 
 
 def solve_stacks(ctx, backend: str = "b200", count_live: bool = False, perturb_ties: bool = False):
@@ -404,8 +406,10 @@ def solve_stacks(ctx, backend: str = "b200", count_live: bool = False, perturb_t
     g, H = ctx.grids, ctx.horizon
     m = _Marshal(ctx, ctx.steps)
     terminal = _f64(ctx.terminal)
-    J_stack = np.empty((H + 1, g.n_v, g.n_soc, g.n_t))
-    P_stack = np.empty((H, g.n_v, g.n_soc, g.n_t), dtype=np.int32)
+    # page-locked output blocks (recycled): the levels arrive by direct DMA
+    # while the remaining stages still sweep
+    J_stack = _abi.PINNED.array((H + 1, g.n_v, g.n_soc, g.n_t), np.float64)
+    P_stack = _abi.PINNED.array((H, g.n_v, g.n_soc, g.n_t), np.int32)
     st = _abi.EcoStats()
     _abi.check(_abi.lib().eco_solve_horizon(
         C.byref(m.plant), C.byref(m.prob), m.plans, H, _abi.ptr(terminal, C.c_double),

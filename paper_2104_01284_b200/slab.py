@@ -126,6 +126,27 @@ class SlabSolver:
             pass
 
 
+def emulate_slabs(ctx, world: int, backend: str = "b200"):
+    """The ``world``-rank slab decomposition of one solve emulated on ONE GPU
+    (eco_slab_emulate): every rank's replica of the J stack, (world, H + 1,
+    n_v, n_soc, n_t), and the policy stack assembled from the slabs.  GPU-count
+    invariance (test_parallel.py:164-171) means every replica equals the
+    unpartitioned solve_horizon."""
+    g, H = ctx.grids, ctx.horizon
+    part = make_partition(g.n_v, world)
+    bounds = np.array([lo for lo, _ in part] + [g.n_v], dtype=np.int32)
+    m = _Marshal(ctx, ctx.steps)
+    terminal = _f64(ctx.terminal)
+    J = np.empty((world, H + 1, g.n_v, g.n_soc, g.n_t))
+    P = np.empty((H, g.n_v, g.n_soc, g.n_t), dtype=np.int32)
+    st = _abi.EcoStats()
+    _abi.check(_abi.lib().eco_slab_emulate(world, _abi.ptr(bounds, C.c_int32), precision_of(backend),
+                                           C.byref(m.plant), C.byref(m.prob), m.plans, H,
+                                           _abi.ptr(terminal, C.c_double), _abi.ptr(J, C.c_double),
+                                           _abi.ptr(P, C.c_int32), C.byref(st)), "eco_slab_emulate")
+    return J, P, st.as_dict()
+
+
 def gather_policies(res: SlabResult, n_v: int, dst: int = 0, group=None) -> Optional[np.ndarray]:
     """Assemble the full (H, n_v, n_soc, n_t) policy stack on rank ``dst``
     from every rank's slab (host transport of the process group)."""
@@ -143,4 +164,4 @@ def gather_policies(res: SlabResult, n_v: int, dst: int = 0, group=None) -> Opti
     return out
 
 
-__all__ = ["SlabSolver", "SlabResult", "make_partition", "gather_policies", "EXCHANGES"]
+__all__ = ["SlabSolver", "SlabResult", "make_partition", "gather_policies", "emulate_slabs", "EXCHANGES"]

@@ -323,17 +323,47 @@ def test_c3_fine_grid_fp64_bitwise_vs_oracle(c3_short_ctx):
         assert np.array_equal(P[k], Po[k]), k
 
 
-def test_c3_fine_grid_fp32_tolerance_full_horizon(vehicle, urban_route):
-    """C3 at the full H = 20: the fp32 production build against the fp64
-    build (bitwise to the oracle above) at every level."""
-    from paper_2104_01284_b200.dp import solve_stacks
+@pytest.fixture(scope="module")
+def c3_full_ctx(vehicle, urban_route):
     route, spat = urban_route
-    ctx = build_context(vehicle, route, spat, 60, 30.0, grids=C3_GRID, penalty=PEN, gamma=0.5, horizon=20)
-    J64, P64, _ = solve_stacks(ctx, "b200-fp64")
-    J32, P32, st = solve_stacks(ctx, "b200", count_live=True)
-    assert st["stages"] == 20 and st["live_updates"] > 0
+    return build_context(vehicle, route, spat, 60, 30.0, grids=C3_GRID, penalty=PEN, gamma=0.5, horizon=20)
+
+
+def test_c3_full_horizon_fp64_bitwise_vs_reference(c3_full_ctx):
+    """C3 at the full H = 20 against the REFERENCE's own solve
+    (solve_horizon(backend="parallel"), tests/golden/make_golden.py c3):
+    blake2b digests of all 21 J and 20 P levels equal."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    g = golden_json("c3_urban_s60_t30.json")
+    J, P, st = solve_stacks(c3_full_ctx, "b200-fp64")
+    assert st["stages"] == 20
+    for k in range(21):
+        assert table_digest(J[k]) == g["J"][k], f"J level {k}"
     for k in range(20):
-        mask, p999, mx, pol = fp32_agreement(J32[k], P32[k], J64[k], P64[k])
+        assert table_digest(P[k]) == g["P"][k], f"P level {k}"
+
+
+def test_c3_full_horizon_fp32_within_tolerance_vs_reference(c3_full_ctx):
+    """The fp32 production build at C3, every level, against the reference's
+    values: finite counts and sums of every level, and the stated tolerances
+    on 16,384 seeded state samples per level (golden c3 samples)."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    g = golden_json("c3_urban_s60_t30.json")
+    smp = golden_npz("c3_urban_s60_t30_samples.npz")
+    idx = smp["idx"]
+    J, P, st = solve_stacks(c3_full_ctx, "b200", count_live=True)
+    assert st["live_updates"] > 0
+    for k in range(21):
+        lvl = g["levels"][k]
+        fin = J[k] < PEN.j_inf
+        n_fin = int(fin.sum())
+        assert abs(n_fin - lvl["finite"]) <= 1e-3 * lvl["finite"], (k, n_fin, lvl["finite"])
+        s = float(J[k][fin].sum())
+        assert abs(s - lvl["sum_finite"]) <= 1e-4 * lvl["sum_finite"], (k, s, lvl["sum_finite"])
+        Js = J[k].reshape(-1)[idx]
+        Pk = P[k].reshape(-1)[idx] if k < 20 else np.zeros_like(idx, dtype=np.int32)
+        Pr = smp["P"][k] if k < 20 else np.zeros_like(idx, dtype=np.int32)
+        mask, p999, mx, pol = fp32_agreement(Js, Pk, smp["J"][k], Pr)
         assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (k, mask, p999, mx, pol)
 
 
