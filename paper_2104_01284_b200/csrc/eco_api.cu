@@ -272,6 +272,15 @@ void launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t st, bool 
 // long time ladders take the wide-row stage path (ECO_WIDE=0 disables it)
 inline bool wide_rows(int nt) { return nt >= 128 && nt % 2 == 0 && env_int("ECO_WIDE", 1) != 0; }
 
+// wide rows in row blocks (bellman_wide2_kernel, ECO_WIDE2=0 disables it):
+// warps per row block (kW2S states each), 0 when not used
+inline int w2_wpr(int nt) {
+    if (!wide_rows(nt) || env_int("ECO_WIDE2", 1) == 0) return 0;
+    const int wpr = (nt + kW2S - 1) / kW2S;
+    return wpr <= kW2MaxWarps ? wpr : 0;
+}
+inline int w2_tj(int nt) { return w2_wpr(nt) ? kW2R : 0; }
+
 // --------------------------------------------------------- geometry store
 template <typename Real>
 struct Geometry {
@@ -346,8 +355,9 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     }
     // staging plans of the (v, soc, t) stage kernel's tiles
     const int upr = (g.nt + kZP - 1) / kZP;
-    const int tj_default = G.tj_pref > 0 ? G.tj_pref : (wide_rows(g.nt) ? 2 : std::max(1, 16 / upr));
-    G.tj = std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", tj_default)));
+    const int tj_default = G.tj_pref > 0 ? G.tj_pref
+                                          : (w2_tj(g.nt) ? w2_tj(g.nt) : (wide_rows(g.nt) ? 2 : std::max(1, 16 / upr)));
+    G.tj = w2_tj(g.nt) ? std::min(g.nx, tj_default) : std::min(g.nx, std::max(1, env_int("ECO_TILE_TJ", tj_default)));
     G.nchunk = (g.nx + G.tj - 1) / G.tj;
     // wide-row tiles never stage a band (and get no RowRec2 buffer): cap -1
     // marks every one of them unstaged
@@ -412,6 +422,20 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode, bool alias = false) 
     } else {
         t.tj = G.tj;
         t.nchunk = G.nchunk;
+        if (w2_wpr(nt)) {
+            // row blocks: one warp per (kW2R rows, kW2S states), every warp
+            // scans all actions (no slices); the reduction buffers only serve
+            // the per-state path of standstill tiles (S = block, 1 slice)
+            t.wide = w2_wpr(nt);
+            t.S = 32 * t.wide;
+            t.slices = 1;
+            t.count_max = std::max(1, G.h_gmax[0]);
+            // the band region holds the per-action W2Quad summaries
+            t.band_cap = (int)((t.count_max * sizeof(W2Quad<Real>) + sizeof(Real) - 1) / sizeof(Real));
+            t.smem = TileSmem<Real>(nt, t.tj, 1, t.count_max, t.band_cap).total;
+            if (t.smem > 227 * 1024) throw ArgError{"tile buffers exceed shared memory"};
+            return t;
+        }
         if (wide_rows(nt)) {
             // wide rows: S = warps per row x 32 x tj, no shared-memory staging
             t.wide = (nt + 64 * kMW - 1) / (64 * kMW);
@@ -506,7 +530,8 @@ template <typename Real>
 int light_first(const Geometry<Real>& G, int nt, int nlaunch) {
     if (env_int("ECO_LIGHT_FIRST", 1) == 0) return 0;
     const TileCfg tc = tile_cfg(G, nt, 0);
-    auto k = tc.wide ? bellman_wide_kernel<Real, false> : bellman_stage_kernel<Real, false>;
+    auto k = (tc.wide && w2_wpr(nt)) ? bellman_wide2_kernel<Real, false>
+                                     : tc.wide ? bellman_wide_kernel<Real, false> : bellman_stage_kernel<Real, false>;
     set_smem_attr(k, tc.smem);
     int per_sm = 0;
     ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, tc.S * tc.slices, tc.smem));
@@ -522,9 +547,14 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
     if (MODE == 0) {
         using KT = void (*)(StageArgs<Real>);
         KT k;
+        const bool w2 = tc.wide && w2_wpr(a.nt);
         if (rev) {   // perturb_ties (highest index wins ties): plain solves only
             if (count || a.npeer > 0) throw ArgError{"perturb_ties: not with live counting or slab exchange"};
-            k = tc.wide ? bellman_wide_kernel<Real, false, false, true> : bellman_stage_kernel<Real, false, false, true>;
+            k = w2 ? bellman_wide2_kernel<Real, false, false, true>
+                   : tc.wide ? bellman_wide_kernel<Real, false, false, true> : bellman_stage_kernel<Real, false, false, true>;
+        } else if (w2) {
+            k = a.npeer > 0 ? (count ? bellman_wide2_kernel<Real, true, true> : bellman_wide2_kernel<Real, false, true>)
+                            : (count ? bellman_wide2_kernel<Real, true> : bellman_wide2_kernel<Real, false>);
         } else if (a.npeer > 0)
             k = tc.wide ? (count ? bellman_wide_kernel<Real, true, true> : bellman_wide_kernel<Real, false, true>)
                         : (count ? bellman_stage_kernel<Real, true, true> : bellman_stage_kernel<Real, false, true>);
@@ -793,7 +823,14 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     static cudaStream_t ovs = nullptr;
     static std::vector<cudaEvent_t> lvl_ev;
     if (overlap) {
-        if (!ovs) ECO_CUDA(cudaStreamCreateWithFlags(&ovs, cudaStreamNonBlocking));
+        if (!ovs) {
+            // highest priority: each level's conversion kernel must not queue
+            // behind the remaining stages' pending CTAs, or the downloads
+            // would trail the whole sweep instead of overlapping it
+            int lo_pri = 0, hi_pri = 0;
+            ECO_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+            ECO_CUDA(cudaStreamCreateWithPriority(&ovs, cudaStreamNonBlocking, hi_pri));
+        }
         while ((int)lvl_ev.size() < H + 1) {
             cudaEvent_t e;
             ECO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -2125,7 +2162,8 @@ void slab_emulate_impl(int nranks, const int32_t* bounds, const EcoPlant* plant,
     if (!peers.empty()) d_peers.upload(peers.data(), peers.size(), st);
     e.peers = d_peers.p;
     const TileCfg tc = tile_cfg(G, nt, 0);
-    auto kern = tc.wide ? bellman_emul_kernel<Real, true> : bellman_emul_kernel<Real, false>;
+    auto kern = (tc.wide && w2_wpr(nt)) ? bellman_emul_kernel<Real, true, true>
+                                         : tc.wide ? bellman_emul_kernel<Real, true> : bellman_emul_kernel<Real, false>;
     set_smem_attr(kern, tc.smem);
     EventTimer all;
     all.start(st);

@@ -714,7 +714,111 @@ __device__ __forceinline__ bool improves(Real F, Real best) {
     else return F < best;
 }
 
-template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false, bool PREFETCH = false, bool REV = false>
+// ---- wide rows, row blocks (W2): a warp owns kW2R consecutive source SoC
+// rows x kW2S consecutive ladder states and scans ALL the plane's actions
+// (no slice merge).  For one action the kW2R rows land on consecutive
+// destination rows (xi' = xi - dt*I/C_nom shifts every row alike: checked per
+// action, else a per-row path), so kW2R + 1 destination rows per speed corner
+// serve all kW2R source rows from registers: 10 row loads instead of 16.
+constexpr int kW2R = 4;        // source rows per warp (= per CTA)
+constexpr int kW2S = 63;       // ladder states per warp: 64 samples (2 per lane), the last state
+                               // dropped (its t' + 1 sample sits in the next warp's range)
+
+// Per (tile, action) summary built in the CTA prologue: base = the (ivlo,
+// jxlo, zoff) index of row 0 when the fast path applies (all kW2R rows on the
+// hull, consecutive destination rows, non-degenerate SoC and speed cells),
+// else -1; wx = the rows' SoC weights.  Kept in the tile's (unused) band region.
+template <typename Real>
+struct alignas(8) W2Quad {
+    int32_t base, pad;
+    Real wx[kW2R];
+};
+
+// One warp's action scan over its kW2R rows x kW2S states (W2).  best / bk
+// index r * 2 + i.  RED: the stage has red arrival samples.
+template <typename Real, bool COUNT, bool REV, bool RED>
+__device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<Real>* __restrict__ s_ro,
+                                        const ActRec<Real>* __restrict__ s_act, const W2Quad<Real>* __restrict__ s_q,
+                                        const uint8_t* __restrict__ s_green, int count, int nr, int zs,
+                                        Real (&best)[2 * kW2R], int (&bk)[2 * kW2R], unsigned long long& nlive) {
+    using PR = Pair<Real>;
+    using V2 = typename Vec2<Real>::T;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int nt = a.nt, plane = a.nx * nt, tj = a.tj;
+    const int z0 = zs + 2 * lane;                            // the lane's two states z0, z0 + 1
+    const bool keep1 = lane != 31;                           // state zs + 63: next warp's t' + 1 sample
+    const Real* __restrict__ J0 = a.J_next;
+    const Real* __restrict__ J1 = a.J_next1;
+    for (int k = 0; k < count; ++k) {
+        const ActRec<Real> rc = s_act[k];
+        const int zoff = (int)(rc.meta & kRecZoff);
+        const bool dzh = (rc.meta & kRecDzh) != 0;
+        const int zl = nt - 1 - zoff - (dzh ? 1 : 0);       // last live state of every valid row
+        if (zs > zl) continue;                               // warp-uniform
+        const bool gated = RED && (rc.meta & kRecGated) != 0;
+        const Real wv = rc.wv, wz = rc.wz, c1 = rc.c1;
+        const bool ok0 = z0 <= zl && (!gated || s_green[min(z0 + zoff, nt - 1)] != 0);           // K:516
+        const bool ok1 = keep1 && z0 + 1 <= zl && (!gated || s_green[min(z0 + 1 + zoff, nt - 1)] != 0);
+        // t-blend (K:361) of the SoC-blended pair + lexicographic update; the
+        // pair's second state takes its t' + 1 sample from the next lane
+        auto update = [&](int r, PR col) {
+            const Real nxt = __shfl_down_sync(full, col.x, 1);
+            PR f = col;
+            if (dzh) f = p_lerp(col, PR{col.y, nxt}, wz);
+            f = p_addc(f, c1);
+            if (COUNT) nlive += ok0 + ok1;
+            const bool u0 = ok0 && improves<REV>(f.x, best[2 * r]);
+            const bool u1 = ok1 && improves<REV>(f.y, best[2 * r + 1]);
+            best[2 * r] = u0 ? f.x : best[2 * r];
+            bk[2 * r] = u0 ? k : bk[2 * r];
+            best[2 * r + 1] = u1 ? f.y : best[2 * r + 1];
+            bk[2 * r + 1] = u1 ? k : bk[2 * r + 1];
+        };
+        const W2Quad<Real> qd = s_q[k];
+        if (qd.base >= 0) {
+            // kW2R + 1 consecutive destination rows, speed-blended once and
+            // shared by the kW2R source rows (the reference's lerp tree:
+            // v inside, then SoC, K:335-337)
+            const unsigned base = (unsigned)(qd.base + zs);
+            const Real* p = ((base & 1u) ? J1 : J0) + (base & ~1u) + 2 * lane;
+            V2 tl[kW2R + 1], th[kW2R + 1];
+#pragma unroll
+            for (int q = 0; q <= kW2R; ++q) {
+                tl[q] = __ldg(reinterpret_cast<const V2*>(p + q * nt));
+                th[q] = __ldg(reinterpret_cast<const V2*>(p + q * nt + plane));
+            }
+            PR vb[kW2R + 1];
+#pragma unroll
+            for (int q = 0; q <= kW2R; ++q) vb[q] = p_lerp(PR{tl[q].x, tl[q].y}, PR{th[q].x, th[q].y}, wv);
+#pragma unroll
+            for (int r = 0; r < kW2R; ++r) update(r, p_lerp(vb[r], vb[r + 1], qd.wx[r]));
+        } else {
+            // rows off the SoC hull, a degenerate SoC / speed cell, or a tail
+            // block: each row its own corners (hi = lo where degenerate)
+            const int dv = (rc.meta & kRecDvh) ? plane : 0;
+#pragma unroll
+            for (int r = 0; r < kW2R; ++r) {
+                if (r >= nr) break;
+                const RowRec<Real> ro = s_ro[k * tj + r];
+                if (ro.off < 0) continue;                    // warp-uniform
+                const unsigned off = (unsigned)(ro.off + zs);
+                const Real* b00 = ((off & 1u) ? J1 : J0) + (off & ~1u) + 2 * lane;
+                const int dx = ro.wx > (Real)0 ? nt : 0;
+                const V2 t00 = __ldg(reinterpret_cast<const V2*>(b00));
+                const V2 t10 = __ldg(reinterpret_cast<const V2*>(b00 + dv));
+                const V2 t01 = __ldg(reinterpret_cast<const V2*>(b00 + dx));
+                const V2 t11 = __ldg(reinterpret_cast<const V2*>(b00 + dx + dv));
+                const PR lo = p_lerp(PR{t00.x, t00.y}, PR{t10.x, t10.y}, wv);
+                const PR hi = p_lerp(PR{t01.x, t01.y}, PR{t11.x, t11.y}, wv);
+                update(r, p_lerp(lo, hi, ro.wx));
+            }
+        }
+    }
+}
+
+template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false, bool PREFETCH = false, bool REV = false,
+          bool W2 = false>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
@@ -965,6 +1069,79 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 s_arg[slice * tj_nt + r * nt + z] = bk[i];
             }
         }
+    } else if (W2 && fast) {
+        // ---- row blocks (see kW2R): records to shared memory first
+        RowRec<Real>* s_ro = reinterpret_cast<RowRec<Real>*>(smem + L.rr);
+        {
+            constexpr int ro16 = sizeof(RowRec<Real>) / 16, act16 = sizeof(ActRec<Real>) / 16;
+            for (int i = threadIdx.x; i < count * tja * ro16; i += blockDim.x) {
+                const int e = i / ro16, h = i - e * ro16;
+                const int k = e / tja, rr = e - k * tja;
+                cp_async16(reinterpret_cast<char*>(s_ro + k * a.tj + rr) + 16 * h,
+                           reinterpret_cast<const char*>(rows + (size_t)k * nx + rr) + 16 * h);
+            }
+            for (int i = threadIdx.x; i < count * act16; i += blockDim.x)
+                cp_async16(reinterpret_cast<char*>(s_act) + 16 * i, reinterpret_cast<const char*>(acts) + 16 * i);
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        W2Quad<Real>* s_q = reinterpret_cast<W2Quad<Real>*>(smem + L.band);
+        for (int k = threadIdx.x; k < count; k += blockDim.x) {
+            const RowRec<Real>* rk = s_ro + k * a.tj;
+            W2Quad<Real> q;
+            bool f = tja == kW2R && (s_act[k].meta & kRecDvh) != 0;
+#pragma unroll
+            for (int r = 0; r < kW2R; ++r) {
+                const RowRec<Real> ro = r < tja ? rk[r] : RowRec<Real>{-1, -1, (Real)0, 0};
+                q.wx[r] = ro.wx;
+                f = f && ro.wx > (Real)0 && ro.off == rk[0].off + r * nt;
+            }
+            q.base = f ? rk[0].off : -1;
+            q.pad = 0;
+            s_q[k] = q;
+        }
+        pdl_wait();
+        __syncthreads();
+        if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int nr = min(kW2R, tja);                       // rows of this tile
+        const int zs = warp * kW2S;                          // first ladder state of the warp
+        const int z0 = zs + 2 * lane;
+        Real best[2 * kW2R];
+        int bk[2 * kW2R];
+#pragma unroll
+        for (int i = 0; i < 2 * kW2R; ++i) { best[i] = a.j_inf; bk[i] = -1; }
+        if (zs < nt) {
+            if (any_red) w2_scan<Real, COUNT, REV, true>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
+            else w2_scan<Real, COUNT, REV, false>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
+        }
+        // results straight from registers: every state has one owner thread
+        if (COUNT && a.live) {
+            unsigned long long w = nlive;
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
+            if (lane == 0 && w) atomicAdd(a.live, w);
+        }
+#pragma unroll
+        for (int r = 0; r < kW2R; ++r) {
+            if (r >= nr) break;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int z = z0 + i;
+                if (z >= nt || z >= zs + kW2S) continue;
+                const size_t f = obase + (size_t)r * nt + z;
+                const int b = bk[2 * r + i];
+                const Real val = b < 0 ? (Real)INFINITY : best[2 * r + i];
+                a.J_out[f] = val;
+                if (a.J_out1 && f > 0) a.J_out1[f - 1] = val;
+                if (PEERS) store_peers(a, f, val);
+                if (a.P_out) a.P_out[f] = b < 0 ? -1 : (int)(s_act[b].meta >> kRecUShift);
+            }
+        }
+        if (dbg) {
+            __syncthreads();
+            if (threadIdx.x == 0) { dbg[2] = dbg[3] = gtimer(); dbg[4] = smid(); dbg[5] = (unsigned long long)count * tja; }
+        }
+        return;
     } else if (WIDE && fast) {
         // the tile's row records and the plane's action records go to shared
         // memory first (route geometry: no dependency on the previous stage),
@@ -1345,6 +1522,21 @@ bellman_wide_kernel(StageArgs<Real> a) {
     stage_tile<Real, COUNT, true, PEERS, false, REV>(a, blockIdx.x, smem);
 }
 
+// Row-block variant of the wide-row kernel (W2, see kW2R): one CTA = kW2R
+// source rows of a plane x the whole ladder, a warp per kW2S states, no
+// slice merge.
+#ifndef ECO_W2_MINB
+#define ECO_W2_MINB 4
+#endif
+constexpr int kW2MaxWarps = 7;   // n_t <= 7 * kW2S = 441 (longer ladders: bellman_wide_kernel)
+template <typename Real, bool COUNT, bool PEERS = false, bool REV = false>
+__global__ void __launch_bounds__(32 * kW2MaxWarps, ECO_W2_MINB)
+bellman_wide2_kernel(StageArgs<Real> a) {
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char smem[];
+    stage_tile<Real, COUNT, true, PEERS, false, REV, true>(a, blockIdx.x, smem);
+}
+
 // Single-GPU emulation of a G-rank slab stage (tests of the C5 exchange on a
 // one-GPU lease, where ranks whose kernels wait on one another cannot run as
 // separate launches): ONE launch covers every rank's tiles; a CTA of a tile
@@ -1362,8 +1554,8 @@ struct EmulArgs {
     int nranks;
 };
 
-template <typename Real, bool WIDE>
-__global__ void __launch_bounds__(256, WIDE ? ECO_WIDE_MINB : ECO_STAGE_MINB)
+template <typename Real, bool WIDE, bool W2 = false>
+__global__ void __launch_bounds__(W2 ? 32 * kW2MaxWarps : 256, W2 ? ECO_W2_MINB : WIDE ? ECO_WIDE_MINB : ECO_STAGE_MINB)
 bellman_emul_kernel(StageArgs<Real> a, EmulArgs<Real> e) {
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1377,7 +1569,7 @@ bellman_emul_kernel(StageArgs<Real> a, EmulArgs<Real> e) {
     a.peer_base = e.peers + (size_t)g * (e.nranks - 1);
     a.npeer = e.nranks - 1;
     a.peer_off = e.out_off;
-    stage_tile<Real, false, WIDE, true, !WIDE>(a, blockIdx.x, smem);
+    stage_tile<Real, false, WIDE, true, !WIDE, false, W2>(a, blockIdx.x, smem);
 }
 
 // Batch of independent solves sharing one route's geometry (run_bench's

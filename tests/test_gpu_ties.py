@@ -73,3 +73,37 @@ def test_perturbed_ties_wide_rows(vehicle, urban_route):
         assert np.array_equal(x.values, y.values)
     for x, y in zip(a.policies, b.policies):
         assert np.array_equal(x.values < 0, y.values < 0) and np.all(y.values >= x.values)
+
+
+def test_concurrent_solves_from_two_threads(vehicle, short_route, urban_route):
+    """The stateless solvers share one device workspace: calls from two host
+    threads (ctypes releases the GIL) serialise on its mutex and return
+    uncorrupted tables (advisor finding, round 1)."""
+    import threading
+    route, spat = short_route
+    uroute, uspat = urban_route
+    ctx_a = build_context(vehicle, route, spat, 45, 50.0, grids=GridSpec(n_v=12, n_soc=8, n_t=40),
+                          penalty=PenaltyConfig(), gamma=0.5, horizon=20)
+    ctx_b = build_context(vehicle, uroute, uspat, 60, 30.0, grids=GridSpec(), penalty=PenaltyConfig(), gamma=0.5,
+                          horizon=20)
+    ref_a = solve_horizon(ctx_a, backend="b200-fp64")
+    ref_b = solve_horizon(ctx_b, backend="b200-fp64")
+    errors = []
+
+    def worker(ctx, ref):
+        try:
+            for _ in range(6):
+                res = solve_horizon(ctx, backend="b200-fp64")
+                for x, y in zip(res.tables, ref.tables):
+                    assert np.array_equal(x.values, y.values)
+                for x, y in zip(res.policies, ref.policies):
+                    assert np.array_equal(x.values, y.values)
+        except Exception as exc:         # pragma: no cover - reported below
+            errors.append(exc)
+
+    th = [threading.Thread(target=worker, args=(ctx_a, ref_a)), threading.Thread(target=worker, args=(ctx_b, ref_b))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
