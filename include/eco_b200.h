@@ -199,6 +199,12 @@ int32_t eco_release_workspace(void);
  * remaining stages still sweep.  Any output pointer may also be ordinary
  * pageable memory. */
 int32_t eco_host_alloc(uint64_t bytes, void** out);
+/* Checked builds (-DECO_CHECKED, paper_2104_01284_b200/_eco_b200_checked.so):
+ * violations counted since the last reset -- gathers of J_{k+1} / of a tile's
+ * shared-memory band outside their buffers, and stage outputs not written
+ * exactly once (the single-writer rule).  Regular builds
+ * report -1 for both. */
+int32_t eco_debug_checks(int64_t* bounds_violations, int64_t* writer_violations, int32_t reset);
 int32_t eco_host_free(void* p);
 
 /* One backward Bellman step (backward_step, dp.py:365-404).  J_next, J_out

@@ -226,6 +226,7 @@ def _declare(lib):
         "eco_device_count": (_I, []),
         "eco_release_workspace": (_I, []),
         "eco_host_alloc": (_I, [C.c_uint64, P(C.c_void_p)]),
+        "eco_debug_checks": (_I, [P(C.c_int64), P(C.c_int64), _I]),
         "eco_host_free": (_I, [C.c_void_p]),
         "eco_bellman_step": (_I, [P(EcoPlant), P(EcoProblem), P(EcoStepPlan), P(EcoStage1Tables),
                                   _PD, _PD, _PI, _I, _I, P(EcoStats)]),

@@ -379,7 +379,12 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     // records); the per-tile kernel remains for grids whose chunk tables
     // exceed shared memory
     const size_t psmem = ((size_t)3 * G.nchunk * g.nv + G.nchunk) * sizeof(int32_t);
-    if (psmem <= 200 * 1024 && env_int("ECO_PLANE_TILES", 1) != 0) {
+    if (wide_rows(g.nt)) {
+        const size_t nt_ = ntiles;
+        geom_tile_headers_kernel<<<(unsigned)((nt_ + 255) / 256), 256, 0, st>>>(G.count.p, G.row_off.p, g, G.tj,
+                                                                              G.nchunk, G.tiles.p, G.rank_of.p,
+                                                                              d_plans, d_vaxes, G.gmax.p);
+    } else if (psmem <= 200 * 1024 && env_int("ECO_PLANE_TILES", 1) != 0) {
         if (psmem > 48 * 1024)
             ECO_CUDA(cudaFuncSetAttribute(geom_plane_tiles_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)psmem));
@@ -637,6 +642,33 @@ struct TablesDev {
     }
 };
 
+// Checked builds: per-stage single-writer shadow counts (see ECO_CHECKED in
+// eco_kernels.cuh).  arm() before a stage, verify() after it.
+struct WriterCheck {
+#ifdef ECO_CHECKED
+    DBuf<unsigned> cnt;
+    size_t n = 0;
+    explicit WriterCheck(size_t ns) : n(ns) {
+        cnt.alloc(ns);
+        unsigned* p = cnt.p;
+        ECO_CUDA(cudaMemcpyToSymbol(g_chk_wcount, &p, sizeof p));
+    }
+    ~WriterCheck() {
+        unsigned* p = nullptr;
+        cudaMemcpyToSymbol(g_chk_wcount, &p, sizeof p);
+    }
+    void arm(cudaStream_t st) { ECO_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(unsigned), st)); }
+    void verify(cudaStream_t st) {
+        chk_single_writer_kernel<<<grid_for(n), 256, 0, st>>>(cnt.p, n);
+        ECO_CUDA(cudaGetLastError());
+    }
+#else
+    explicit WriterCheck(size_t) {}
+    void arm(cudaStream_t) {}
+    void verify(cudaStream_t) {}
+#endif
+};
+
 // --------------------------------------------------------- horizon solve
 // Per-solve inputs of a horizon solve: plant, the H step plans (DevPlan +
 // source speed axis + ladders + stage flags + source kinds), the axes and the
@@ -838,9 +870,11 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         }
         ECO_CUDA(cudaEventRecord(lvl_ev[H], st));       // the terminal level is in place
     }
+    WriterCheck wchk(ns);
     sweep.start(st);
     for (int k = H - 1; k >= 0; --k) {
         const TileCfg& tc = tcs[k];
+        wchk.arm(st);
         StageArgs<Real> a = tabs ? stage_args(toyG[k], 0, in.v + (size_t)k * nv, nt, tc)
                                  : stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
         a.green = in.green + (size_t)k * nt;
@@ -850,6 +884,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         a.flags = in.flags + k;
         a.J_next = d_J.p + (size_t)(k + 1) * LV;
         a.J_next1 = a.J_next + LC;
+        a.lc = LC;
         a.J_out = d_J.p + (size_t)k * LV;
         a.J_out1 = a.J_out + LC;
         a.P_out = d_P.p + (size_t)k * ns;
@@ -866,6 +901,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             a.dbg = dbgbuf.p;
         }
         launch_stage<Real, 0>(a, tc, count, st, -1, rev);
+        wchk.verify(st);
         if (overlap) ECO_CUDA(cudaEventRecord(lvl_ev[k], st));
         if (dbg_on) {
             std::vector<unsigned long long> h(dbgbuf.n);
@@ -1454,6 +1490,7 @@ struct Session : SessionBase {
                     a.wait = wait.p + (size_t)k * nt;
                     a.J_next = Js + (size_t)(k + 1) * LV;
                     a.J_next1 = a.J_next + LC;
+                    a.lc = LC;
                     a.J_out = Js + (size_t)k * LV;
                     // the shifted copy only serves unstaged tiles (global-memory pair loads)
                     a.J_out1 = ctx.G.all_staged ? nullptr : a.J_out + LC;
@@ -1542,6 +1579,7 @@ struct Session : SessionBase {
                     a.wait = wait.p + (size_t)k * nt;
                     a.J_next = Js + (size_t)(k + 1) * LV;
                     a.J_next1 = a.J_next + LC;
+                    a.lc = LC;
                     a.J_out = Js + (size_t)k * LV;
                     a.J_out1 = G.all_staged ? nullptr : a.J_out + LC;
                     a.P_out = nullptr;
@@ -2071,6 +2109,7 @@ struct Slab : SlabBase {
             a.wait = in.wait + (size_t)k * nt;
             a.J_next = J.p + (size_t)(k + 1) * LV;
             a.J_next1 = a.J_next + LC;
+            a.lc = LC;
             a.J_out = J.p + (size_t)k * LV;
             a.J_out1 = a.J_out + LC;
             // the kernel indexes P by the global state: shift the slab buffer
@@ -2166,8 +2205,10 @@ void slab_emulate_impl(int nranks, const int32_t* bounds, const EcoPlant* plant,
                                          : tc.wide ? bellman_emul_kernel<Real, true> : bellman_emul_kernel<Real, false>;
     set_smem_attr(kern, tc.smem);
     EventTimer all;
+    WriterCheck wchk(ns);
     all.start(st);
     for (int k = H - 1; k >= 0; --k) {
+        wchk.arm(st);
         StageArgs<Real> a = stage_args(G, k, in.v + (size_t)k * nv, nt, tc);
         a.green = in.green + (size_t)k * nt;
         a.flags = in.flags + k;
@@ -2184,6 +2225,7 @@ void slab_emulate_impl(int nranks, const int32_t* bounds, const EcoPlant* plant,
         e.out_off = (size_t)k * LV;
         kern<<<nv * tc.nchunk, tc.S * tc.slices, tc.smem, st>>>(a, e);
         ECO_CUDA(cudaGetLastError());
+        wchk.verify(st);
         ++launches;
         for (int g = 0; g < nranks; ++g) {
             shift_copy_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(e.rep[g] + (size_t)k * LV, ns, LC);
@@ -2234,6 +2276,29 @@ int32_t eco_release_workspace(void) {
         std::lock_guard<std::mutex> lock(workspace_mutex());
         horizon_workspace<float>().release();
         horizon_workspace<double>().release();
+    });
+}
+
+int32_t eco_debug_checks(int64_t* bounds_violations, int64_t* writer_violations, int32_t reset) {
+    return run_guarded([&] {
+        if (!bounds_violations || !writer_violations) throw ArgError{"null pointer argument"};
+#ifdef ECO_CHECKED
+        ECO_CUDA(cudaDeviceSynchronize());
+        unsigned long long b = 0, w = 0;
+        ECO_CUDA(cudaMemcpyFromSymbol(&b, g_chk_bounds, sizeof b));
+        ECO_CUDA(cudaMemcpyFromSymbol(&w, g_chk_writer, sizeof w));
+        *bounds_violations = (int64_t)b;
+        *writer_violations = (int64_t)w;
+        if (reset) {
+            const unsigned long long z = 0;
+            ECO_CUDA(cudaMemcpyToSymbol(g_chk_bounds, &z, sizeof z));
+            ECO_CUDA(cudaMemcpyToSymbol(g_chk_writer, &z, sizeof z));
+        }
+#else
+        (void)reset;
+        *bounds_violations = -1;
+        *writer_violations = -1;
+#endif
     });
 }
 

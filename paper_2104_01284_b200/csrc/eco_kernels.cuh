@@ -447,6 +447,33 @@ geom_plane_tiles_kernel(PairGeom<Real> g, GeomDims d, int tj, int nchunk, int ba
     }
 }
 
+// Tile headers only (wide-row grids: the stage kernels stage no band, so the
+// footprint / segment plan of geom_plane_tiles_kernel is not needed): one
+// thread per (plan, plane, SoC chunk).
+__global__ void geom_tile_headers_kernel(const int32_t* __restrict__ count, const int64_t* __restrict__ row_off,
+                                         GeomDims d, int tj, int nchunk, TilePlan* __restrict__ tiles,
+                                         const int32_t* __restrict__ rank_of, const DevPlan* __restrict__ plans,
+                                         const double* __restrict__ vaxes, int32_t* __restrict__ gmax) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t per_plan = (size_t)d.nv * nchunk;
+    if (i >= (size_t)d.P * per_plan) return;
+    const int p = (int)(i / per_plan);
+    const int rem = (int)(i - (size_t)p * per_plan);
+    const int iv = rem / nchunk, c = rem - iv * nchunk;
+    const size_t pi = (size_t)p * d.nv + iv;
+    const double v = vaxes[pi];
+    TilePlan* tp = tiles + (size_t)p * per_plan + rank_of[i];
+    tp->iv = iv;
+    tp->j0 = c * tj;
+    tp->tja = min(tj, d.nx - c * tj);
+    tp->count = (plans[p].src_kind == ECO_NODE_STOP && v > 0.0) ? 0 : count[pi];   // K:458-459
+    tp->moving = v > 0.0;
+    tp->row_off = row_off[pi];
+    tp->nseg = -1;
+    tp->band = 0;
+    if (i == 0) atomicOr(&gmax[1], 1);
+}
+
 // per plan: tiles heaviest first -- planes by descending feasible-action
 // count (ties by plane index), the SoC chunks of a plane consecutively.  The
 // order only balances the load; results do not depend on it.
@@ -630,6 +657,39 @@ __device__ __forceinline__ unsigned smid() {
     return r;
 }
 
+// ---- checked build (-DECO_CHECKED, _eco_b200_checked.so): compute-sanitizer
+// is closed on this pool, so the library checks itself.  Every stage output
+// element bumps a shadow counter (the reference SPEC's single-writer rule,
+// each output cell has exactly one owner per stage), and every
+// gather of J_{k+1} / of the shared-memory band is bounds-checked (a
+// violation is counted and the access is not made).
+#ifdef ECO_CHECKED
+__device__ unsigned long long g_chk_bounds = 0;
+__device__ unsigned long long g_chk_writer = 0;
+__device__ unsigned* g_chk_wcount = nullptr;
+__device__ __forceinline__ void chk_write(size_t f) {
+    if (g_chk_wcount) atomicAdd(g_chk_wcount + f, 1u);
+}
+// [p, p + n) inside [lo, lo + extent) (elements)
+template <typename T>
+__device__ __forceinline__ bool chk_in(const T* p, int n, const T* lo, size_t extent) {
+    const bool ok = p >= lo && (size_t)(p - lo) + (size_t)n <= extent;
+    if (!ok) atomicAdd(&g_chk_bounds, 1ull);
+    return ok;
+}
+__global__ void chk_single_writer_kernel(const unsigned* __restrict__ wcount, size_t n) {
+    unsigned long long bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        bad += wcount[i] != 1u;
+    if (bad) atomicAdd(&g_chk_writer, bad);
+}
+#define ECO_CHK_WRITE(f) chk_write(f)
+#define ECO_CHK_IN(p, n, lo, ext) chk_in((p), (n), (lo), (ext))
+#else
+#define ECO_CHK_WRITE(f) ((void)0)
+#define ECO_CHK_IN(p, n, lo, ext) true
+#endif
+
 #ifndef ECO_WIDE_CHUNKS
 #define ECO_WIDE_CHUNKS 4
 #endif
@@ -638,6 +698,7 @@ __device__ __forceinline__ unsigned smid() {
 #endif
 constexpr int kMW = ECO_WIDE_CHUNKS;   // wide path: 64-state chunks per warp
 
+constexpr int kBandPad = 8;   // elements after a tile's band: the fast path's reads past a row's end
 template <typename Real>
 struct TileSmem {
     size_t green, red_best, red_arg, rr, act, band, total;
@@ -658,7 +719,7 @@ struct TileSmem {
             red_arg = o;  o = align16(o + red_a);
             rr = o;       o = align16(o + rr_bytes);
             act = o;      o = align16(o + (size_t)count_max * sizeof(ActRec<Real>));
-            band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
+            band = o;     o = align16(o + (size_t)(band_cap + kBandPad) * sizeof(Real));
             total = o;
             return;
         }
@@ -669,7 +730,7 @@ struct TileSmem {
         const size_t red_end = o;
         o = r0;
         rr = o;       o = align16(o + rr_bytes);
-        band = o;     o = align16(o + (size_t)band_cap * sizeof(Real));
+        band = o;     o = align16(o + (size_t)(band_cap + kBandPad) * sizeof(Real));
         total = o > red_end ? o : red_end;
     }
 };
@@ -783,6 +844,7 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
             const unsigned base = (unsigned)(qd.base + zs);
             const Real* p = ((base & 1u) ? J1 : J0) + (base & ~1u) + 2 * lane;
             V2 tl[kW2R + 1], th[kW2R + 1];
+            if (!ECO_CHK_IN(p, kW2R * nt + plane + 2, J0, 2 * a.lc)) continue;
 #pragma unroll
             for (int q = 0; q <= kW2R; ++q) {
                 tl[q] = __ldg(reinterpret_cast<const V2*>(p + q * nt));
@@ -805,6 +867,7 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
                 const unsigned off = (unsigned)(ro.off + zs);
                 const Real* b00 = ((off & 1u) ? J1 : J0) + (off & ~1u) + 2 * lane;
                 const int dx = ro.wx > (Real)0 ? nt : 0;
+                if (!ECO_CHK_IN(b00, dx + dv + 2, J0, 2 * a.lc)) continue;
                 const V2 t00 = __ldg(reinterpret_cast<const V2*>(b00));
                 const V2 t10 = __ldg(reinterpret_cast<const V2*>(b00 + dv));
                 const V2 t01 = __ldg(reinterpret_cast<const V2*>(b00 + dx));
@@ -838,6 +901,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         pdl_wait();
         for (int f = threadIdx.x; f < tstates; f += blockDim.x) {
             a.J_out[obase + f] = (Real)INFINITY;
+            ECO_CHK_WRITE(obase + f);
             if (a.J_out1 && obase + f > 0) a.J_out1[obase + f - 1] = (Real)INFINITY;
             if (a.P_out) a.P_out[obase + f] = -1;
             if (PEERS) store_peers(a, obase + f, (Real)INFINITY);
@@ -1003,6 +1067,11 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 const Real* plo = s_band + ro.blo + zq;          // (ivlo, jxlo, t' = z0 + zoff)
                 const Real* phi = s_band + ro.bhi + zq;          // (ivhi, jxlo, t')
                 const int dx = ro.wx > (Real)0 ? nt : 0;
+                // memory safety: inside the band allocation (band_cap + the
+                // kBandPad slack; lanes past a row's last live state read a few
+                // samples beyond the staged band, which the masks discard)
+                if (!ECO_CHK_IN(plo, dx + 6, s_band, (size_t)a.band_cap + kBandPad) ||
+                    !ECO_CHK_IN(phi, dx + 6, s_band, (size_t)a.band_cap + kBandPad)) continue;
                 // fp32: one weighted corner sum per t pair with the stage
                 // cost folded in (it cancels in the time blend): 4 FFMA2
                 // instead of 3 lerps + an add.  fp64: the reference's lerp
@@ -1132,6 +1201,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 const int b = bk[2 * r + i];
                 const Real val = b < 0 ? (Real)INFINITY : best[2 * r + i];
                 a.J_out[f] = val;
+                ECO_CHK_WRITE(f);
                 if (a.J_out1 && f > 0) a.J_out1[f - 1] = val;
                 if (PEERS) store_peers(a, f, val);
                 if (a.P_out) a.P_out[f] = b < 0 ? -1 : (int)(s_act[b].meta >> kRecUShift);
@@ -1193,6 +1263,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 const int dx = ro.wx > (Real)0 ? nt : 0;
                 const unsigned off = (unsigned)ro.off;       // (ivlo, jxlo, t' = zoff)
                 const Real* b00 = ((off & 1u) ? J1 : J0) + (off & ~1u) + zb;
+                if (!ECO_CHK_IN(b00, dv + dx + 64 * kMW + 2, J0, 2 * a.lc)) continue;
                 const Real* b10 = b00 + dv;
                 const Real* b01 = b00 + dx;
                 const Real* b11 = b01 + dv;
@@ -1334,6 +1405,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 const unsigned i0 = (unsigned)(ro.off + z0);     // (ivlo, jxlo, t' = z0 + zoff)
                 // all four corner rows share the parity of i0 (plane, nt even)
                 const Real* base = ((i0 & 1u) ? J1 : J0) + (i0 & ~1u);
+                if (!ECO_CHK_IN(base, (int)(dv + dx) + 6, J0, 2 * a.lc)) continue;
                 PR c[4][3];                                      // [corner row][t pair]
                 const unsigned offs[4] = {0u, dv, dx, dv + dx};
 #pragma unroll
@@ -1486,6 +1558,7 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         if (!live) continue;
         const Real val = bk < 0 ? (Real)INFINITY : best;
         a.J_out[obase + f] = val;
+        ECO_CHK_WRITE(obase + f);
         if (a.J_out1 && obase + f > 0) a.J_out1[obase + f - 1] = val;
         if (PEERS) store_peers(a, obase + f, val);
         if (a.P_out) a.P_out[obase + f] = bk < 0 ? -1 : (staged ? (int)(s_act[bk].meta >> kRecUShift) : u[bk]);
@@ -1621,6 +1694,7 @@ bellman_batch_kernel(BatchArgs<Real> ba) {
     Real* Jb = ba.J + (size_t)b * 2 * ba.LV;
     a.J_next = Jb + ((k + 1) & 1) * ba.LV;
     a.J_next1 = a.J_next + ba.LC;
+    a.lc = ba.LC;
     a.J_out = Jb + (k & 1) * ba.LV;
     a.J_out1 = a.J_out + ba.LC;
     a.P_out = (k == 0 && ba.P0) ? ba.P0 + (size_t)b * a.nv * a.nx * a.nt : nullptr;

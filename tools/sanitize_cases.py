@@ -1,7 +1,11 @@
-"""Small device runs for compute-sanitizer (memcheck / racecheck / synccheck):
-every kernel family of the library on tiny inputs, through the public API.
+"""Device runs of every kernel family through the public API, for the
+self-checking build (compute-sanitizer is closed on this pool):
 
-    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
+    ECO_B200_LIB=paper_2104_01284_b200/_eco_b200_checked.so python tools/sanitize_cases.py
+
+prints the checked build's counters (gathers outside their buffers, stage
+outputs not written exactly once) and exits 1 if either is nonzero; with the
+regular build it only exercises the kernels.
 
 Covers: toy tables (narrow stage kernel, per-state path), C1 (signal, red
 wait), perturb_ties, a wide-row context (bellman_wide2_kernel + its per-state
@@ -62,3 +66,16 @@ with BatchSolver(veh, urban, grids=GridSpec(n_v=10, n_soc=8, n_t=40), penalty=pe
                  backend="b200") as bs:
     bs.solve([uspat] * len(sched), sched)
 print("batch ok", flush=True)
+# full-size stage kernels: C2 (narrow, staged band) and C3 (row blocks)
+c2 = build_context(veh, urban, uspat, 60, 30.0, grids=GridSpec(), penalty=pen, gamma=0.5, horizon=4)
+solve_horizon(c2, backend="b200")
+c3 = build_context(veh, urban, uspat, 60, 30.0, grids=GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2), penalty=pen,
+                   gamma=0.5, horizon=2)
+solve_horizon(c3, backend="b200")
+print("full-size stages ok", flush=True)
+import ctypes as C  # noqa: E402
+from paper_2104_01284_b200 import _abi  # noqa: E402
+b, w = C.c_int64(0), C.c_int64(0)
+_abi.check(_abi.lib().eco_debug_checks(C.byref(b), C.byref(w), 1), "eco_debug_checks")
+print(f"checks bounds_violations={b.value} writer_violations={w.value}", flush=True)
+sys.exit(1 if (b.value > 0 or w.value > 0) else 0)
