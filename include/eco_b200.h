@@ -345,6 +345,11 @@ int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant,
                        int32_t H, const double* terminal, double* J_stack,
                        int32_t* P_slab, int32_t count_live, EcoStats* stats);
 int32_t eco_slab_destroy(EcoSlab* slab);
+/* ECO_XCHG_P2P with several ranks on ONE GPU (tests): replace the GPU-side
+ * stage barrier by a stream sync + barrier(user) on the host (e.g. a gloo
+ * barrier), so no kernel waits on another process's kernels.  NULL restores
+ * the GPU barrier. */
+int32_t eco_slab_set_host_barrier(EcoSlab* slab, void (*barrier)(void*), void* user);
 /* The slab decomposition of nranks ranks emulated on ONE GPU (tests of the
  * exchange where fewer GPUs than ranks are available): one launch per stage
  * covers every rank's tiles, each rank keeps its own replica of the levels,

@@ -252,6 +252,7 @@ def _declare(lib):
         "eco_slab_solve": (_I, [C.c_void_p, P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI, _I,
                                 P(EcoStats)]),
         "eco_slab_destroy": (_I, [C.c_void_p]),
+        "eco_slab_set_host_barrier": (_I, [C.c_void_p, C.c_void_p, C.c_void_p]),
         "eco_slab_emulate": (_I, [_I, _PI, _I, P(EcoPlant), P(EcoProblem), P(EcoStepPlan), _I, _PD, _PD, _PI,
                                   P(EcoStats)]),
         "eco_solve_batch": (_I, [P(EcoPlant), P(EcoRoute), P(EcoMpcConfig), _I, C.c_void_p, _PI, _PD, _PD, _PI,

@@ -281,6 +281,27 @@ inline int w2_wpr(int nt) {
 }
 inline int w2_tj(int nt) { return w2_wpr(nt) ? kW2R : 0; }
 
+template <typename K>
+void set_smem_attr(K kernel, size_t smem) {
+    // cached per kernel (keeps attribute calls out of stream capture).  The
+    // attribute is process-wide, so the cache is too and only ever RAISES the
+    // limit: a thread setting a smaller value would invalidate another
+    // thread's launches with a larger one
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> done;
+    if (smem <= 48 * 1024) return;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& d : done)
+        if (d.first == (const void*)kernel) {
+            if (d.second >= smem) return;
+            d.second = smem;
+            ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            return;
+        }
+    ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.emplace_back((const void*)kernel, smem);
+}
+
 // --------------------------------------------------------- geometry store
 template <typename Real>
 struct Geometry {
@@ -342,8 +363,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     G.rows_total = last_off + (int64_t)last_cnt * g.nx;
     if (G.row.cap < (size_t)std::max<int64_t>(1, G.rows_total)) G.row.alloc((size_t)std::max<int64_t>(1, G.rows_total));
     const size_t smem = (size_t)g.ntb * g.nx * (sizeof(double) + 1) + 16;
-    if (smem > 48 * 1024)
-        ECO_CUDA(cudaFuncSetAttribute(geom_soc_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr(geom_soc_kernel<Real>, smem);
     geom_soc_kernel<Real><<<grid, 256, smem, st>>>(d_plant, d_vaxes, d_tb, d_soc, g, G.view(),
                                                    d_tab.ok != nullptr ? 1 : 0);
     ECO_CUDA(cudaGetLastError());
@@ -385,9 +405,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
                                                                               G.nchunk, G.tiles.p, G.rank_of.p,
                                                                               d_plans, d_vaxes, G.gmax.p);
     } else if (psmem <= 200 * 1024 && env_int("ECO_PLANE_TILES", 1) != 0) {
-        if (psmem > 48 * 1024)
-            ECO_CUDA(cudaFuncSetAttribute(geom_plane_tiles_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)psmem));
+        set_smem_attr(geom_plane_tiles_kernel<Real>, psmem);
         geom_plane_tiles_kernel<Real><<<dim3(g.nv, g.P), 256, psmem, st>>>(
             G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
     } else {
@@ -503,21 +521,6 @@ StageArgs<Real> stage_args(Geometry<Real>& G, int p, const double* d_vsrc, int n
     return a;
 }
 
-template <typename K>
-void set_smem_attr(K kernel, size_t smem) {
-    // cached per kernel: keeps attribute calls out of stream capture
-    static thread_local std::vector<std::pair<const void*, size_t>> done;
-    if (smem <= 48 * 1024) return;
-    for (auto& d : done)
-        if (d.first == (const void*)kernel) {
-            if (d.second >= smem) return;
-            d.second = smem;
-            ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            return;
-        }
-    ECO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done.emplace_back((const void*)kernel, smem);
-}
 
 inline int sm_count_cached() {
     static int n = 0;
@@ -1939,6 +1942,7 @@ struct SlabBase {
     virtual void connect(const unsigned char* all) = 0;
     virtual void solve(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H,
                        const double* terminal, double* J_stack, int32_t* P_slab, int count, EcoStats* stats) = 0;
+    virtual void set_host_barrier(void (*fn)(void*), void* user) = 0;
 };
 
 template <typename Real>
@@ -1964,6 +1968,23 @@ struct Slab : SlabBase {
     ncclUniqueId nid{};
     bool connected = false;
     cudaStream_t st = 0;
+    // host-side stage barrier (tests of the P2P data path with several ranks
+    // on ONE GPU, where a GPU-side spin barrier across processes may not be
+    // used): stream sync + the caller's barrier instead of slab_barrier_kernel
+    void (*host_barrier)(void*) = nullptr;
+    void* host_barrier_user = nullptr;
+
+    void gpu_or_host_barrier() {
+        ++barriers;
+        if (host_barrier) {
+            ECO_CUDA(cudaStreamSynchronize(st));
+            host_barrier(host_barrier_user);
+            return;
+        }
+        slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
+                                              (unsigned)(barriers * nranks), err.p);
+        ECO_CUDA(cudaGetLastError());
+    }
 
     Slab(int nranks_, int rank_, int exchange_, const int32_t* bounds, int nv_, int nx_, int nt_, int Hmax_)
         : nranks(nranks_), rank(rank_), exchange(exchange_), Hmax(Hmax_), nv(nv_), nx(nx_), nt(nt_) {
@@ -1997,6 +2018,11 @@ struct Slab : SlabBase {
         for (Real* p : peer_J) cudaIpcCloseMemHandle(p);
         for (unsigned* p : peer_flag) cudaIpcCloseMemHandle(p);
         if (st) cudaStreamDestroy(st);
+    }
+
+    void set_host_barrier(void (*fn)(void*), void* user) override {
+        host_barrier = fn;
+        host_barrier_user = user;
     }
 
     void info(unsigned char* out) override {
@@ -2047,10 +2073,7 @@ struct Slab : SlabBase {
         Real* Lk = J.p + (size_t)k * LV;
         const size_t plane = (size_t)nx * nt;
         if (exchange == ECO_XCHG_P2P) {
-            ++barriers;
-            slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
-                                                  (unsigned)(barriers * nranks), err.p);
-            ECO_CUDA(cudaGetLastError());
+            gpu_or_host_barrier();
         } else {
             const ncclDataType_t ty = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
             if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
@@ -2093,10 +2116,7 @@ struct Slab : SlabBase {
         // P2P: no rank may store into a peer's levels while that peer still
         // reads its previous solve's tables (output conversion, D2H)
         if (exchange == ECO_XCHG_P2P && nranks > 1) {
-            ++barriers;
-            slab_barrier_kernel<<<1, 32, 0, st>>>(d_peer_flag.p, (int)peer_flag.size(), flag.p,
-                                                  (unsigned)(barriers * nranks), err.p);
-            ECO_CUDA(cudaGetLastError());
+            gpu_or_host_barrier();
             ++launches;
         }
         sweep.start(st);
@@ -2526,6 +2546,13 @@ int32_t eco_slab_solve(EcoSlab* slab, const EcoPlant* plant, const EcoProblem* p
         if (!slab || !plans || !terminal) throw ArgError{"null pointer argument"};
         reinterpret_cast<SlabBase*>(slab)->solve(plant, prob, plans, H, terminal, J_stack, P_slab, count_live,
                                                  stats);
+    });
+}
+
+int32_t eco_slab_set_host_barrier(EcoSlab* slab, void (*barrier)(void*), void* user) {
+    return run_guarded([&] {
+        if (!slab) throw ArgError{"null pointer argument"};
+        reinterpret_cast<SlabBase*>(slab)->set_host_barrier(barrier, user);
     });
 }
 

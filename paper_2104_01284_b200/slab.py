@@ -64,7 +64,13 @@ class SlabSolver:
     process group constructs it and calls :meth:`solve` with the same context)."""
 
     def __init__(self, n_v: int, n_soc: int, n_t: int, max_horizon: int, *, backend: str = "b200",
-                 exchange: str = "p2p", rank: Optional[int] = None, world: Optional[int] = None, group=None):
+                 exchange: str = "p2p", rank: Optional[int] = None, world: Optional[int] = None, group=None,
+                 host_barrier: bool = False):
+        """``host_barrier`` (tests): close each P2P stage with a stream sync +
+        a barrier of the process group on the host instead of the GPU-side
+        flag barrier, so several ranks can share ONE GPU (their kernels must
+        not wait on one another there); the data path -- CUDA IPC replicas,
+        epilogue stores into peers, local copy-1 rebuild -- is unchanged."""
         if exchange not in EXCHANGES:
             raise ValueError(f"unknown exchange {exchange!r} (p2p | nccl)")
         dist = _dist()
@@ -90,6 +96,16 @@ class SlabSolver:
             dist.all_gather_object(infos, bytes(info), group=group)
         allinfo = (C.c_uint8 * (_abi.SLAB_INFO_BYTES * world)).from_buffer_copy(b"".join(infos))
         _abi.check(self._lib.eco_slab_connect(self._h, allinfo), "eco_slab_connect")
+        self._barrier_cb = None
+        if host_barrier and world > 1:
+            grp = group
+
+            def _barrier(_user):
+                dist.barrier(group=grp)
+
+            self._barrier_cb = C.CFUNCTYPE(None, C.c_void_p)(_barrier)
+            _abi.check(self._lib.eco_slab_set_host_barrier(self._h, C.cast(self._barrier_cb, C.c_void_p), None),
+                       "eco_slab_set_host_barrier")
 
     def solve(self, ctx, *, return_J: bool = False, return_P: bool = True, count_live: bool = False) -> SlabResult:
         g = ctx.grids
