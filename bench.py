@@ -456,6 +456,9 @@ def run_c4(args, rank, world, local_rank):
                    "precision": args.precision},
         "ms_per_solve": t_max / args.steps / (args.scenarios / world),
         "geometry_ms": fit["device_ms"] - fit["dominant_ms"],
+        "geometry": "the route geometry (one plan per spatial step, shared by every scenario) is built once per "
+                    "BatchSolver, before the timed region, and excluded from value and e2e; geometry_ms is its "
+                    "device time",
         "dense_updates_per_step": total_dense / args.steps, "live_updates_per_step_rank0": live,
         "gpu_launches": int(launches),
         "e2e": {"value": total_dense / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,

@@ -341,10 +341,13 @@ int light_first(const Geometry<Real>& G, int nt, int nlaunch);
 // rebuilds of the same route, so refits allocate nothing).
 // with_tiles = false: pair + SoC-row records only (what the terminal-field
 // sweep reads), no stage-kernel tile plans.
+// staged_flag: read back whether every tile stages its band (G.all_staged,
+// used by the closed loop to skip the shifted level copy) -- one more host
+// round trip, skipped by the stateless solves.
 template <typename Real>
 void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d_plans, const double* d_vaxes,
                     const double* d_te, const double* d_tb, const double* d_soc, const EcoStage1Tables& d_tab,
-                    cudaStream_t st, int64_t* launches, bool with_tiles = true) {
+                    cudaStream_t st, int64_t* launches, bool with_tiles = true, bool staged_flag = true) {
     const GeomDims& g = G.dims;
     if (G.act.n != (size_t)g.P * g.nv * g.U) G.alloc(g.P, g.nv, g.U);
     ECO_CUDA(cudaMemsetAsync(G.gmax.p, 0, 4 * sizeof(int32_t), st));
@@ -414,9 +417,13 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
             G.view(), g, G.tj, G.nchunk, G.band_cap, G.tiles.p, G.row2.p, G.rank_of.p, d_plans, d_vaxes);
     }
     ECO_CUDA(cudaGetLastError());
-    ECO_CUDA(cudaMemcpyAsync(&G.h_gmax[1], G.gmax.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    ECO_CUDA(cudaStreamSynchronize(st));
-    G.all_staged = G.h_gmax[1] == 0 && !wide_rows(g.nt);
+    if (staged_flag) {
+        ECO_CUDA(cudaMemcpyAsync(&G.h_gmax[1], G.gmax.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        ECO_CUDA(cudaStreamSynchronize(st));
+        G.all_staged = G.h_gmax[1] == 0 && !wide_rows(g.nt);
+    } else {
+        G.all_staged = false;
+    }
     if (launches) *launches += 6;
 }
 
@@ -831,7 +838,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
     EventTimer all, sweep;
     all.start(st);
     // toy mode: each step has its own table; geometry built per plan below
-    if (!tabs) build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+    if (!tabs) build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches, true, false);
     to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(in.terminal, d_J.p + (size_t)H * LV, ns, pr->j_inf);
     ECO_CUDA(cudaGetLastError());
     ++launches;
@@ -2108,7 +2115,7 @@ struct Slab : SlabBase {
         G.plo = plo;
         G.phi = phi;
         TablesDev tdev;
-        build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+        build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches, true, false);
         to_internal2_kernel<Real><<<grid_for(ns + 8), 256, 0, st>>>(in.terminal, J.p + (size_t)H * LV, ns, pr->j_inf);
         ECO_CUDA(cudaGetLastError());
         ++launches;
@@ -2200,7 +2207,7 @@ void slab_emulate_impl(int nranks, const int32_t* bounds, const EcoPlant* plant,
     Geometry<Real> G;
     G.dims = GeomDims{H, nv, nx, nt, U, pr->n_te, pr->n_tb, pr->delta_d, pr->a_min, pr->a_max, pr->gamma, pr->dtg};
     TablesDev tdev;
-    build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches);
+    build_geometry(G, in.plant, in.plans, in.v, in.te, in.tb, in.soc, tdev.view, st, &launches, true, false);
     DBuf<Real> rep((size_t)nranks * (H + 1) * LV);
     DBuf<int32_t> P((size_t)H * ns);
     EmulArgs<Real> e{};

@@ -315,13 +315,37 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+_PLANT_CACHE: dict = {}
+
+
+def _plant_of(pack) -> "_abi.EcoPlant":
+    """EcoPlant of a PlantPack, cached by identity (a Vehicle keeps one pack;
+    the cache holds the pack, so its id cannot be reused while cached)."""
+    hit = _PLANT_CACHE.get(id(pack))
+    if hit is not None and hit[0] is pack:
+        return hit[1]
+    if len(_PLANT_CACHE) > 64:
+        _PLANT_CACHE.clear()
+    plant = _abi.pack_plant(pack)
+    _PLANT_CACHE[id(pack)] = (pack, plant)
+    return plant
+
+
+# EcoStepPlan as a numpy record (the plans of a solve are filled vectorised;
+# ctypes pointer objects per field cost ~4 us each)
+_PLAN_DTYPE = np.dtype([("node", "<i4"), ("src_kind", "<i4"), ("dest_kind", "<i4"), ("reserved", "<i4"),
+                        ("grade", "<f8"), ("v0_dest", "<f8"), ("dv_dest", "<f8"), ("cos_grade", "<f8"),
+                        ("sin_grade", "<f8"), ("v_src", "<u8"), ("arr_green", "<u8"), ("dep_ok", "<u8"),
+                        ("t_dep", "<u8"), ("wait", "<u8")])
+assert _PLAN_DTYPE.itemsize == C.sizeof(_abi.EcoStepPlan)
+
+
 class _Marshal:
     """ctypes views of a SolveContext (keeps every numpy buffer alive)."""
 
     def __init__(self, ctx: SolveContext, steps: Sequence[StepPlan]):
         g = ctx.grids
-        self.keep = []
-        self.plant = _abi.pack_plant(ctx.pack)
+        self.plant = _plant_of(ctx.pack)
         self.te, self.tb = _f64(ctx.te_axis), _f64(ctx.tb_axis)
         self.soc, self.tax = _f64(ctx.soc_axis), _f64(ctx.t_axis)
         self.prob = _abi.EcoProblem(
@@ -331,17 +355,31 @@ class _Marshal:
             t0=float(ctx.t_axis[0]), dtg=float(g.dt),
             te_axis=_abi.ptr(self.te, C.c_double), tb_axis=_abi.ptr(self.tb, C.c_double),
             soc_axis=_abi.ptr(self.soc, C.c_double), t_axis=_abi.ptr(self.tax, C.c_double))
-        self.plans = (_abi.EcoStepPlan * len(steps))()
-        for i, p in enumerate(steps):
-            arrs = (_f64(p.v_src), np.ascontiguousarray(p.arr_green, dtype=np.uint8),
-                    np.ascontiguousarray(p.dep_ok, dtype=np.uint8), _f64(p.t_dep), _f64(p.wait))
-            self.keep.append(arrs)
-            self.plans[i] = _abi.EcoStepPlan(
-                node=p.node, src_kind=p.src_kind, dest_kind=p.dest_kind, grade=p.grade,
-                v0_dest=p.v0_dest, dv_dest=p.dv_dest, cos_grade=math.cos(p.grade), sin_grade=math.sin(p.grade),
-                v_src=_abi.ptr(arrs[0], C.c_double), arr_green=_abi.ptr(arrs[1], C.c_uint8),
-                dep_ok=_abi.ptr(arrs[2], C.c_uint8), t_dep=_abi.ptr(arrs[3], C.c_double),
-                wait=_abi.ptr(arrs[4], C.c_double))
+        n = len(steps)
+        # the plans' arrays stacked into one block each; per-plan pointers by
+        # address arithmetic
+        self.v = np.ascontiguousarray(np.stack([p.v_src for p in steps]), dtype=np.float64)
+        self.green = np.ascontiguousarray(np.stack([p.arr_green for p in steps]), dtype=np.uint8)
+        self.dep = np.ascontiguousarray(np.stack([p.dep_ok for p in steps]), dtype=np.uint8)
+        self.tdep = np.ascontiguousarray(np.stack([p.t_dep for p in steps]), dtype=np.float64)
+        self.wait = np.ascontiguousarray(np.stack([p.wait for p in steps]), dtype=np.float64)
+        rec = np.zeros(n, dtype=_PLAN_DTYPE)
+        rec["node"] = [p.node for p in steps]
+        rec["src_kind"] = [p.src_kind for p in steps]
+        rec["dest_kind"] = [p.dest_kind for p in steps]
+        grade = np.array([p.grade for p in steps], dtype=np.float64)
+        rec["grade"] = grade
+        rec["v0_dest"] = [p.v0_dest for p in steps]
+        rec["dv_dest"] = [p.dv_dest for p in steps]
+        # libm cos / sin (road_load's trig is not recomputed on the device)
+        rec["cos_grade"] = [math.cos(float(x)) for x in grade]
+        rec["sin_grade"] = [math.sin(float(x)) for x in grade]
+        idx = np.arange(n, dtype=np.uint64)
+        for field, arr in (("v_src", self.v), ("arr_green", self.green), ("dep_ok", self.dep),
+                           ("t_dep", self.tdep), ("wait", self.wait)):
+            rec[field] = np.uint64(arr.ctypes.data) + idx * np.uint64(arr.strides[0])
+        self.rec = rec
+        self.plans = rec.ctypes.data_as(C.POINTER(_abi.EcoStepPlan))
 
 
 def backward_step(ctx: SolveContext, k: int, J_next: np.ndarray, *, backend: str = "b200",

@@ -4,8 +4,10 @@ routes with seeded signal programs, and the seeded solve schedule.
 These regenerate, value for value, the reference's synthetic inputs
 (fixtures.py:32-251 and bench_schedule bench.py:76-94) so that benchmark and
 parity workloads are the configurations BASELINE.json names.  Equality with
-the reference generators is checked in tests/test_fixtures.py (in the build
-container, where the reference is importable) and through committed digests.
+the reference generators is checked indirectly: every golden fixture under
+tests/golden/ was produced by the reference from ITS generators, and the
+tests rebuild the same inputs here and match those outputs bit for bit
+(tests/test_oracle_golden.py, tests/test_gpu_parity.py).
 """
 
 from __future__ import annotations

@@ -149,6 +149,29 @@ def loop_urban():
     }, indent=1))
 
 
+def c4_all():
+    """All 4096 C4 scenarios (route_i = urban seed i, bench_schedule seed i):
+    digests of each scenario's start-node J / P levels from the reference's
+    parallel backend, plus the finite count and finite sum of J0 (for the
+    fp32 tolerance checks)."""
+    vehicle = make_vehicle()
+    out = []
+    t0 = time.perf_counter()
+    for i in range(4096):
+        route, spat = load_route(make_route_urban(seed=i))
+        s, t = bench_schedule(route, 20, 1, seed=i)[0]
+        ctx = build_context(vehicle, route, spat, s, t, grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20)
+        res = solve_horizon(ctx, backend="parallel", workers=8)
+        J0 = res.tables[0].values
+        fin = J0 < PEN.j_inf
+        out.append([i, int(s), float(t), table_digest(J0), table_digest(res.policies[0].values), int(fin.sum()),
+                    float(J0[fin].sum())])
+        if i % 256 == 0:
+            print(f"c4 {i} {time.perf_counter() - t0:.0f}s", flush=True)
+    (HERE / "c4_all_digests.json").write_text(json.dumps(
+        {"fields": ["seed", "s", "t_start", "J0", "P0", "J0_finite", "J0_sum_finite"], "rows": out}))
+
+
 C3_GRID = dict(n_v=350, n_soc=260, n_t=400, dt=0.2)
 C3_SAMPLES = 16384
 
@@ -272,7 +295,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     jobs = [("primitives", primitives), ("toys", toys), ("c1", c1), ("fields", fields), ("loop_short", loop_short),
-            ("c2", c2_digests), ("c4", c2_batch_seeds), ("c3", c3), ("loop_c3", loop_c3)]
+            ("c2", c2_digests), ("c4", c2_batch_seeds), ("c3", c3), ("loop_c3", loop_c3), ("c4_all", c4_all)]
     if not a.skip_urban_loop:
         jobs.append(("loop_urban", loop_urban))
     for name, fn in jobs:

@@ -23,8 +23,8 @@ for backend in ("b200", "b200-fp64"):
         term = dp._f64(ctx.terminal)
         g, H = ctx.grids, ctx.horizon
         t1 = time.perf_counter()
-        J = np.empty((H + 1, g.n_v, g.n_soc, g.n_t))
-        P = np.empty((H, g.n_v, g.n_soc, g.n_t), dtype=np.int32)
+        J = _abi.PINNED.array((H + 1, g.n_v, g.n_soc, g.n_t), np.float64)
+        P = _abi.PINNED.array((H, g.n_v, g.n_soc, g.n_t), np.int32)
         t2 = time.perf_counter()
         st = _abi.EcoStats()
         _abi.check(_abi.lib().eco_solve_horizon(C.byref(m.plant), C.byref(m.prob), m.plans, H,
