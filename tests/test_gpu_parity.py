@@ -423,6 +423,45 @@ def test_c4_batch_fp32_tolerance(vehicle):
     assert mask >= 0.999 and p999 <= REL_P999 and mx <= REL_MAX and pol >= 0.999, (mask, p999, mx, pol)
 
 
+@pytest.fixture(scope="module")
+def c4_all():
+    from conftest import GOLDEN
+    if not (GOLDEN / "c4_all_digests.json").exists():
+        pytest.skip("C4 all-scenario golden not generated")
+    g = golden_json("c4_all_digests.json")
+    routes, sched = _c4_scenarios(len(g["rows"]))
+    assert [(r[1], r[2]) for r in g["rows"]] == [(int(s), float(t)) for s, t in sched]
+    return g["rows"], routes, sched
+
+
+def test_c4_all_4096_scenarios_fp64_vs_reference(vehicle, c4_all):
+    """All 4096 C4 scenarios in one batch against the REFERENCE's own
+    solve_horizon(backend="parallel") per scenario: J0 / P0 digests equal."""
+    from paper_2104_01284_b200.batch import BatchSolver
+    rows, routes, sched = c4_all
+    with BatchSolver(vehicle, routes[0][0], grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20,
+                     backend="b200-fp64") as bs:
+        res = bs.solve([sp for _, sp in routes], sched)
+    bad = [r[0] for i, r in enumerate(rows)
+           if table_digest(res.J0[i]) != r[3] or table_digest(res.P0[i]) != r[4]]
+    assert not bad, bad[:20]
+
+
+def test_c4_all_4096_scenarios_fp32_vs_reference(vehicle, c4_all):
+    """The fp32 batch against the reference: every scenario's J0 finite count
+    within 0.1 % and finite sum within 1e-4 of the reference's."""
+    from paper_2104_01284_b200.batch import BatchSolver
+    rows, routes, sched = c4_all
+    with BatchSolver(vehicle, routes[0][0], grids=GridSpec(), penalty=PEN, gamma=0.5, horizon=20,
+                     backend="b200") as bs:
+        res = bs.solve([sp for _, sp in routes], sched)
+    for i, r in enumerate(rows):
+        fin = res.J0[i] < PEN.j_inf
+        n, ssum = int(fin.sum()), float(res.J0[i][fin].sum())
+        assert abs(n - r[5]) <= 1e-3 * max(1, r[5]), (i, n, r[5])
+        assert abs(ssum - r[6]) <= 1e-4 * max(1.0, r[6]), (i, ssum, r[6])
+
+
 def test_c4_batch_terminal_field_and_no_teleport(vehicle):
     """Options of build_context: the offline terminal field and teleport=False."""
     from paper_2104_01284_b200.batch import solve_batch
