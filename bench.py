@@ -514,9 +514,15 @@ def c3_context(H=20):
 
 
 def so_digest() -> str:
+    """Identity of the library build: the kernel sources + header + nvcc flags
+    (the .so bytes themselves embed nvcc's per-run temp-file names)."""
     import hashlib
-    from paper_2104_01284_b200 import _abi
-    return hashlib.sha256(_abi.library_path().read_bytes()).hexdigest()[:16]
+    import __graft_entry__ as ge
+    h = hashlib.sha256(" ".join(ge.NVCC_FLAGS).encode())
+    for f in sorted(ge.CSRC.glob("*.cu*")) + [ROOT / "include" / "eco_b200.h"]:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
 
 
 def measured_traffic(key: str):

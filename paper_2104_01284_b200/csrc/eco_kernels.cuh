@@ -781,7 +781,10 @@ __device__ __forceinline__ bool improves(Real F, Real best) {
 // destination rows (xi' = xi - dt*I/C_nom shifts every row alike: checked per
 // action, else a per-row path), so kW2R + 1 destination rows per speed corner
 // serve all kW2R source rows from registers: 10 row loads instead of 16.
-constexpr int kW2R = 4;        // source rows per warp (= per CTA)
+#ifndef ECO_W2R
+#define ECO_W2R 4
+#endif
+constexpr int kW2R = ECO_W2R;  // source rows per warp (= per CTA)
 constexpr int kW2S = 63;       // ladder states per warp: 64 samples (2 per lane), the last state
                                // dropped (its t' + 1 sample sits in the next warp's range)
 

@@ -5,7 +5,7 @@
 # Summaries here afterwards: tools/ncu_report.py, tools/launch_stats.py.
 R=${1:-r02}
 O=gpurun_out
-sha256sum paper_2104_01284_b200/_eco_b200.so | cut -c1-16 > $O/${R}_so_digest.txt
+python -c "import bench; print(bench.so_digest())" > $O/${R}_so_digest.txt
 python -m pytest tests -m gpu -q -x > $O/${R}_pytest_gpu.log 2>&1; tail -2 $O/${R}_pytest_gpu.log
 python bench.py > $O/${R}_bench_c3.json 2> $O/${R}_bench_c3.err; tail -c 300 $O/${R}_bench_c3.json
 python bench.py --impl reference --steps 20 --warmup 3 > $O/${R}_bench_ref.json 2> $O/${R}_bench_ref.err; tail -c 200 $O/${R}_bench_ref.json
