@@ -36,10 +36,13 @@ lines = [f"kernel: {d.get('Kernel Name', ('?',))[0]}",
          f"{d['launch__registers_per_thread'][0]} regs"]
 lines.append(f"DRAM read+write per launch: {dram / 1e9:.3f} GB ({dram / dur / 1e9:.0f} GB/s)"
              + (f"; algorithmic {algo / 1e9:.3f} GB (x{dram / algo:.2f})" if algo else ""))
-for name, label in (("lts__t_bytes.sum", "L2 traffic"), ("l1tex__t_bytes.sum", "L1 traffic")):
+for name, label, scale in (("lts__t_bytes.sum", "L2 traffic", 1), ("lts__t_sectors.sum", "L2 traffic", 32),
+                           ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 reads from the SMs", 32),
+                           ("l1tex__t_bytes.sum", "L1 traffic", 1),
+                           ("SM_B.TriageCompute.l1tex__t_sectors.sum", "L1 traffic", 32)):
     if name in d:
-        b = num(name)[0]
-        lines.append(f"{label}: {b / 1e9:.1f} GB per launch = {b / dur / 1e12:.2f} TB/s")
+        b = num(name)[0] * scale
+        lines.append(f"{label} ({name}): {b / 1e9:.1f} GB per launch = {b / dur / 1e12:.2f} TB/s")
 for name in ("lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
              "l1tex__throughput.avg.pct_of_peak_sustained_active",
              "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
