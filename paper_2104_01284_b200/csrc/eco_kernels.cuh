@@ -794,7 +794,7 @@ constexpr int kW2S = 63;       // ladder states per warp: 64 samples (2 per lane
 // else -1; wx = the rows' SoC weights.  Kept in the tile's (unused) band region.
 template <typename Real>
 struct alignas(8) W2Quad {
-    int32_t base, pad;
+    int32_t base, zl;          // zl: last live ladder state of the action's rows (n_t - 1 - zoff - dzh)
     Real wx[kW2R];
 };
 
@@ -815,11 +815,12 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
     const Real* __restrict__ J0 = a.J_next;
     const Real* __restrict__ J1 = a.J_next1;
     for (int k = 0; k < count; ++k) {
+        const W2Quad<Real> qd = s_q[k];
+        const int zl = qd.zl;                                // last live state of every valid row
+        if (zs > zl) continue;                               // warp-uniform
         const ActRec<Real> rc = s_act[k];
         const int zoff = (int)(rc.meta & kRecZoff);
         const bool dzh = (rc.meta & kRecDzh) != 0;
-        const int zl = nt - 1 - zoff - (dzh ? 1 : 0);       // last live state of every valid row
-        if (zs > zl) continue;                               // warp-uniform
         const bool gated = RED && (rc.meta & kRecGated) != 0;
         const Real wv = rc.wv, wz = rc.wz, c1 = rc.c1;
         const bool ok0 = z0 <= zl && (!gated || s_green[min(z0 + zoff, nt - 1)] != 0);           // K:516
@@ -828,8 +829,11 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
         // pair's second state takes its t' + 1 sample from the next lane
         auto update = [&](int r, PR col) {
             const Real nxt = __shfl_down_sync(full, col.x, 1);
-            PR f = col;
-            if (dzh) f = p_lerp(col, PR{col.y, nxt}, wz);
+            // without a time blend (wz == 0) the pair blends with itself:
+            // lerp(a, a, 0) == a exactly, and the neighbour's sample (maybe
+            // infeasible) is never touched
+            const PR nb{dzh ? col.y : col.x, dzh ? nxt : col.y};
+            PR f = p_lerp(col, nb, wz);
             f = p_addc(f, c1);
             if (COUNT) nlive += ok0 + ok1;
             const bool u0 = ok0 && improves<REV>(f.x, best[2 * r]);
@@ -839,7 +843,6 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
             best[2 * r + 1] = u1 ? f.y : best[2 * r + 1];
             bk[2 * r + 1] = u1 ? k : bk[2 * r + 1];
         };
-        const W2Quad<Real> qd = s_q[k];
         if (qd.base >= 0) {
             // kW2R + 1 consecutive destination rows, speed-blended once and
             // shared by the kW2R source rows (the reference's lerp tree:
@@ -1169,7 +1172,8 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 f = f && ro.wx > (Real)0 && ro.off == rk[0].off + r * nt;
             }
             q.base = f ? rk[0].off : -1;
-            q.pad = 0;
+            const uint32_t m = s_act[k].meta;
+            q.zl = nt - 1 - (int)(m & kRecZoff) - ((m & kRecDzh) ? 1 : 0);
             s_q[k] = q;
         }
         pdl_wait();
