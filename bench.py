@@ -605,8 +605,11 @@ def run_c3(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "e2e": {"value": dense * world / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": int(ns * 8 + 20 * (g.n_v * 8 + g.n_t * (1 + 1 + 8 + 8))),
-                "d2h_bytes_per_step": int(21 * ns * 8 + 20 * ns * 4),
-                "api": "paper_2104_01284_b200.solve_horizon(ctx, backend) -> SolveResult (pinned output pool)"},
+                # fp32: each J level crosses PCIe as f32 and is widened to
+                # the f64 table by host threads; fp64: f64 levels
+                "d2h_bytes_per_step": int(21 * ns * (4 if args.precision == "fp32" else 8) + 20 * ns * 4),
+                "api": "paper_2104_01284_b200.solve_horizon(ctx, backend) -> SolveResult with all 21 f64 J and "
+                       "20 int32 P levels on the host (9.0 GB; pinned output pool)"},
         "roofline": _roofline(args, local_rank, live, sweep_max / args.steps / 1e3, "bellman_wide_kernel",
                               traffic, tsrc, algorithmic_bytes=ns * 4 + 3 * ns * 4),
         "clocks": clk.summary(),

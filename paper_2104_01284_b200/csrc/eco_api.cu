@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <immintrin.h>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -243,6 +244,124 @@ void download_big(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     }
     ECO_CUDA(cudaEventSynchronize(ev[prev]));
     host_copy(out + prev_off, stage[prev], prev_n);
+}
+
+inline int env_int(const char* name, int dflt);
+
+// Level-by-level f32 -> f64 download of a solve's J stack (levels H..0 as
+// their stages finish, lvl_ev[k]) + the int32 policies, through a ring of
+// pinned f32 staging buffers; host threads widen each level into the
+// caller's table (infeasible +inf -> j_inf, the to_external conversion)
+// while the next levels' DMA runs.  Returns when every level is written.
+// f32 -> f64 with infeasible (+inf) -> j_inf over [a, b): streaming
+// (non-temporal) stores, so the f64 table is written without first being
+// read into the cache -- host memory bandwidth is what bounds this copy.
+__attribute__((target("avx2"))) void widen_range_avx2(const float* src, double* dst, size_t a, size_t b,
+                                                      double j_inf) {
+    size_t i = a;
+    for (; i < b && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) {
+        const double x = (double)src[i];
+        dst[i] = x < j_inf ? x : j_inf;
+    }
+    const __m256d cap = _mm256_set1_pd(j_inf);
+    for (; i + 8 <= b; i += 8) {
+        const __m256 v = _mm256_loadu_ps(src + i);
+        // x < j_inf ? x : j_inf  ==  min(x, j_inf) for x finite or +inf
+        const __m256d lo = _mm256_min_pd(_mm256_cvtps_pd(_mm256_castps256_ps128(v)), cap);
+        const __m256d hi = _mm256_min_pd(_mm256_cvtps_pd(_mm256_extractf128_ps(v, 1)), cap);
+        _mm256_stream_pd(dst + i, lo);
+        _mm256_stream_pd(dst + i + 4, hi);
+    }
+    for (; i < b; ++i) {
+        const double x = (double)src[i];
+        dst[i] = x < j_inf ? x : j_inf;
+    }
+    _mm_sfence();
+}
+
+// Levels with widen(k) false go the direct way instead (device-side f64
+// conversion into d_tmp + f64 DMA): mixing the two balances the PCIe link
+// (which the f64 levels load) against host memory bandwidth (which the
+// widening loads: DMA write + read + f64 write per level).
+template <typename WidenPred>
+void widen_levels(const float* d_J, size_t LV, size_t ns, int H, double j_inf, const int32_t* d_P, double* J_stack,
+                  int32_t* P_stack, const std::vector<cudaEvent_t>& lvl_ev, cudaStream_t st, double* d_tmp,
+                  WidenPred widen_level) {
+    constexpr int kSlots = 4;
+    static std::mutex mu;
+    static float* stage[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+    static size_t stage_n = 0;
+    static cudaEvent_t ev[kSlots];
+    std::lock_guard<std::mutex> lock(mu);
+    if (stage_n < ns) {
+        for (int b = 0; b < kSlots; ++b) {
+            if (stage[b]) cudaFreeHost(stage[b]);
+            else ECO_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            ECO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), ns * sizeof(float), cudaHostAllocDefault));
+        }
+        stage_n = ns;
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nthr = (int)std::max(1u, std::min(16u, hw ? hw : 1u));
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    auto widen = [&](const float* src, double* dst) {
+        std::vector<std::thread> th;
+        const size_t per = ((ns + nthr - 1) / nthr + 1023) & ~size_t(1023);
+        for (int t = 0; t < nthr; ++t) {
+            const size_t a = (size_t)t * per;
+            if (a >= ns) break;
+            const size_t b = std::min(ns, a + per);
+            th.emplace_back([=] {
+                if (avx2) widen_range_avx2(src, dst, a, b, j_inf);
+                else
+                    for (size_t i = a; i < b; ++i) {
+                        const double x = (double)src[i];
+                        dst[i] = x < j_inf ? x : j_inf;
+                    }
+            });
+        }
+        for (auto& x : th) x.join();
+    };
+    // the widened levels in completion order; the others are enqueued direct
+    std::vector<int> wl;
+    for (int k = H; k >= 0; --k) {
+        if (!widen_level(k)) continue;
+        wl.push_back(k);
+    }
+    const int L = (int)wl.size();
+    int queued = 0, k_next = H;          // k_next: next level (any kind) to enqueue, in completion order
+    auto enqueue_until = [&](int k_stop) {  // enqueue every level down to (and including) k_stop
+        for (; k_next >= k_stop; --k_next) {
+            const int k = k_next;
+            ECO_CUDA(cudaStreamWaitEvent(st, lvl_ev[k], 0));
+            if (widen_level(k)) {
+                const int b = queued % kSlots;
+                ECO_CUDA(cudaMemcpyAsync(stage[b], d_J + (size_t)k * LV, ns * sizeof(float), cudaMemcpyDeviceToHost,
+                                         st));
+                ECO_CUDA(cudaEventRecord(ev[b], st));
+                ++queued;
+            } else {
+                to_external_levels_kernel<float><<<grid_for(ns), 256, 0, st>>>(d_J + (size_t)k * LV,
+                                                                              d_tmp + (size_t)k * ns, ns, 1, j_inf);
+                ECO_CUDA(cudaGetLastError());
+                ECO_CUDA(cudaMemcpyAsync(J_stack + (size_t)k * ns, d_tmp + (size_t)k * ns, ns * sizeof(double),
+                                         cudaMemcpyDeviceToHost, st));
+            }
+            if (k < H)
+                ECO_CUDA(cudaMemcpyAsync(P_stack + (size_t)k * ns, d_P + (size_t)k * ns, ns * sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, st));
+        }
+    };
+    for (int done = 0; done < L; ++done) {
+        // keep up to kSlots widened levels in flight (and every direct level
+        // in between)
+        const int last = std::min(L - 1, done + kSlots - 1);
+        if (queued <= last) enqueue_until(wl[last]);
+        const int k = wl[done], b = done % kSlots;
+        ECO_CUDA(cudaEventSynchronize(ev[b]));
+        widen(stage[b], J_stack + (size_t)k * ns);
+    }
+    enqueue_until(0);                    // direct levels after the last widened one
 }
 
 inline int env_int(const char* name, int dflt) {
@@ -938,6 +1057,17 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
         // once (the copy engine streams levels out as the sweep produces
         // them); pageable ones go through download_big's staging per level
         const bool direct = host_pinned(J_stack) && host_pinned(P_stack);
+        // fp32 levels cross PCIe as f32 (half the bytes) and are widened to
+        // the caller's f64 tables by host threads, level by level while
+        // later levels are still in flight: the C3 tables are 9 GB as f64 /
+        // int32 and the link (57 GB/s) bounds the solve end to end
+        if (sizeof(Real) == 4 && direct && env_int("ECO_HOST_WIDEN", 1) != 0) {
+            // every level widened measured best (C3 e2e: all 164 ms, every
+            // 2nd 182, none 191): host memory, not the link, bounds the mix
+            const int every = std::max(1, env_int("ECO_WIDEN_EVERY", 1));
+            widen_levels(reinterpret_cast<const float*>(d_J.p), LV, ns, H, pr->j_inf, d_P.p, J_stack, P_stack,
+                         lvl_ev, ovs, d_tmp.p, [&](int k) { return (H - k) % every == 0; });
+        } else
         for (int k = H; k >= 0; --k) {
             ECO_CUDA(cudaStreamWaitEvent(ovs, lvl_ev[k], 0));
             to_external_levels_kernel<Real><<<grid_for(ns), 256, 0, ovs>>>(d_J.p + (size_t)k * LV,
@@ -956,7 +1086,7 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             download_big(J_stack + (size_t)k * ns, d_tmp.p + (size_t)k * ns, ns * sizeof(double), ovs);
             if (k < H) download_big(P_stack + (size_t)k * ns, d_P.p + (size_t)k * ns, ns * sizeof(int32_t), ovs);
         }
-        if (direct) ECO_CUDA(cudaStreamSynchronize(ovs));
+        ECO_CUDA(cudaStreamSynchronize(ovs));
         if (dbg_io) {
             const auto h2 = std::chrono::steady_clock::now();
             std::fprintf(stderr, "io: upload(host) %.2f ms, all %.2f ms, direct=%d, outputs done at %.2f ms after "

@@ -637,3 +637,14 @@ def test_closed_loop_variants_fp32_within_0p1pct(vehicle, kind, seed, gamma):
     fuel_ref = float(np.sum(ref["rows"]["fuel_inc_g"]))
     assert abs(traj.fuel_g - fuel_ref) <= 1e-3 * fuel_ref, (traj.fuel_g, fuel_ref)
     assert abs(traj.final_state.t - ref["final"][2]) <= 1e-3 * ref["final"][2], (traj.final_state.t, ref["final"][2])
+
+
+def test_c3_host_widened_levels_equal_device_conversion(c3_short_ctx, monkeypatch):
+    """Large fp32 solves send each level as f32 and widen it on the host
+    (ECO_HOST_WIDEN): the tables equal the device-side f64 conversion bitwise."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    J1, P1, _ = solve_stacks(c3_short_ctx, "b200")
+    monkeypatch.setenv("ECO_HOST_WIDEN", "0")
+    J0, P0, _ = solve_stacks(c3_short_ctx, "b200")
+    assert np.array_equal(J1, J0) and np.array_equal(P1, P0)
+    assert np.all(J1[J1 >= PEN.j_inf] == PEN.j_inf)
