@@ -202,38 +202,45 @@ geom_soc_kernel(const EcoPlant* __restrict__ plant, const double* __restrict__ v
     const size_t base = pi * g.U;
     const int n = out.count[pi];
     RowRec<Real>* rows = out.row + out.row_off[pi];
-    for (int i = threadIdx.x; i < n * g.nx; i += blockDim.x) {
-        const int k = i / g.nx, jx = i - k * g.nx;
+    // a warp per action, its lanes over the SoC rows (no index divisions;
+    // the action's record is loaded once per warp, the row records it writes
+    // are contiguous)
+    const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int k = threadIdx.x >> 5; k < n; k += nwarp) {
         const int packed = out.u[base + k];
         const int ivlo = packed >> 16;
         const ActRec<Real> a = out.act[base + k];
         const int zoff = (int)(a.meta & kRecZoff);
-        double c;
-        bool okb;
-        if (per_action_pbat) {
-            okb = battery_current(P, out.pbat[base + k], soc_axis[jx], &c);
-        } else {
-            const int itb = (packed & 0xFFFF) % g.ntb;
-            okb = cur_ok[itb * g.nx + jx] != 0;
-            c = cur[itb * g.nx + jx];
-        }
-        RowRec<Real> ro;
-        ro.off = -1;
-        ro.zlim = -1;
-        ro.wx = (Real)0;
-        ro.cell = 0;
-        if (okb) {
-            const double xi2 = soc_axis[jx] - out.dt[base + k] * c / P.c_nom;
-            int lo, hi;
-            double w;
-            if (locate_uniform(xi2, x0, dx, g.nx, &lo, &hi, &w)) {
-                ro.cell = ivlo * g.nx + lo;
-                ro.off = ro.cell * g.nt + zoff;
-                ro.zlim = g.nt - 1 - zoff - ((a.meta & kRecDzh) ? 1 : 0);
-                ro.wx = (Real)w;
+        const int zlim = g.nt - 1 - zoff - ((a.meta & kRecDzh) ? 1 : 0);
+        const double dtk = out.dt[base + k];
+        const int itb = (packed & 0xFFFF) % g.ntb;
+        for (int jx = lane; jx < g.nx; jx += 32) {
+            double c;
+            bool okb;
+            if (per_action_pbat) {
+                okb = battery_current(P, out.pbat[base + k], soc_axis[jx], &c);
+            } else {
+                okb = cur_ok[itb * g.nx + jx] != 0;
+                c = cur[itb * g.nx + jx];
             }
+            RowRec<Real> ro;
+            ro.off = -1;
+            ro.zlim = -1;
+            ro.wx = (Real)0;
+            ro.cell = 0;
+            if (okb) {
+                const double xi2 = soc_axis[jx] - dtk * c / P.c_nom;
+                int lo, hi;
+                double w;
+                if (locate_uniform(xi2, x0, dx, g.nx, &lo, &hi, &w)) {
+                    ro.cell = ivlo * g.nx + lo;
+                    ro.off = ro.cell * g.nt + zoff;
+                    ro.zlim = zlim;
+                    ro.wx = (Real)w;
+                }
+            }
+            rows[(size_t)k * g.nx + jx] = ro;
         }
-        rows[k * g.nx + jx] = ro;
     }
 }
 
