@@ -60,3 +60,19 @@ def test_slab_emulation_rejects_bad_partitions(c2_ctx):
         emulate_slabs(c2_ctx, 9, "b200")              # > 8 emulated ranks
     with pytest.raises(ValueError):
         make_partition(35, 36)
+
+
+def test_slab_ranks_invariant_c3_shape(vehicle, urban_route):
+    """The row-block wide kernel's PEERS epilogue at the real C3 grid
+    (350 x 260 x 400): 4 emulated ranks, 3 stages, every replica bitwise
+    equal to the unpartitioned fp64 solve."""
+    route, spat = urban_route
+    ctx = build_context(vehicle, route, spat, 60, 30.0, grids=GridSpec(n_v=350, n_soc=260, n_t=400, dt=0.2),
+                        penalty=PEN, gamma=0.5, horizon=3)
+    ref = solve_horizon(ctx, backend="b200-fp64")
+    J, P, _ = emulate_slabs(ctx, 4, "b200-fp64")
+    for g in range(4):
+        for k in range(4):
+            assert np.array_equal(J[g, k], ref.tables[k].values), (g, k)
+    for k in range(3):
+        assert np.array_equal(P[k], ref.policies[k].values), k
