@@ -284,9 +284,9 @@ __attribute__((target("avx2"))) void widen_range_avx2(const float* src, double* 
 // (which the f64 levels load) against host memory bandwidth (which the
 // widening loads: DMA write + read + f64 write per level).
 template <typename WidenPred>
-void widen_levels(const float* d_J, size_t LV, size_t ns, int H, double j_inf, const int32_t* d_P, double* J_stack,
-                  int32_t* P_stack, const std::vector<cudaEvent_t>& lvl_ev, cudaStream_t st, double* d_tmp,
-                  WidenPred widen_level) {
+void widen_levels(const float* d_J, size_t LV, size_t ns, int H, int k_top, double j_inf, const int32_t* d_P,
+                  double* J_stack, int32_t* P_stack, const std::vector<cudaEvent_t>& lvl_ev, cudaStream_t st,
+                  double* d_tmp, WidenPred widen_level) {
     constexpr int kSlots = 4;
     static std::mutex mu;
     static float* stage[kSlots] = {nullptr, nullptr, nullptr, nullptr};
@@ -324,12 +324,12 @@ void widen_levels(const float* d_J, size_t LV, size_t ns, int H, double j_inf, c
     };
     // the widened levels in completion order; the others are enqueued direct
     std::vector<int> wl;
-    for (int k = H; k >= 0; --k) {
+    for (int k = k_top; k >= 0; --k) {
         if (!widen_level(k)) continue;
         wl.push_back(k);
     }
     const int L = (int)wl.size();
-    int queued = 0, k_next = H;          // k_next: next level (any kind) to enqueue, in completion order
+    int queued = 0, k_next = k_top;      // k_next: next level (any kind) to enqueue, in completion order
     auto enqueue_until = [&](int k_stop) {  // enqueue every level down to (and including) k_stop
         for (; k_next >= k_stop; --k_next) {
             const int k = k_next;
@@ -923,9 +923,12 @@ HorizonWorkspace<Real>& horizon_workspace() {
 
 // dp.py:425-475 / dp.py:557-610: H plans, terminal -> J stack, P stack.
 template <typename Real>
+// skip_terminal: J_stack receives levels 0..H-1 only (the terminal level is
+// the caller's own input: backward_step's J_next).
 void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoStepPlan* plans, int H,
                         const EcoStage1Tables* tabs, const double* terminal, double* J_stack, int32_t* P_stack,
-                        bool count, EcoStats* stats, bool rev = false) {
+                        bool count, EcoStats* stats, bool rev = false, bool skip_terminal = false) {
+    const int top = skip_terminal ? H - 1 : H;    // highest level returned
     const int nv = pr->n_v, nx = pr->n_soc, nt = pr->n_t, U = pr->n_te * pr->n_tb;
     const size_t ns = (size_t)nv * nx * nt;
     std::lock_guard<std::mutex> lock(workspace_mutex());
@@ -1065,10 +1068,10 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             // every level widened measured best (C3 e2e: all 164 ms, every
             // 2nd 182, none 191): host memory, not the link, bounds the mix
             const int every = std::max(1, env_int("ECO_WIDEN_EVERY", 1));
-            widen_levels(reinterpret_cast<const float*>(d_J.p), LV, ns, H, pr->j_inf, d_P.p, J_stack, P_stack,
+            widen_levels(reinterpret_cast<const float*>(d_J.p), LV, ns, H, top, pr->j_inf, d_P.p, J_stack, P_stack,
                          lvl_ev, ovs, d_tmp.p, [&](int k) { return (H - k) % every == 0; });
         } else
-        for (int k = H; k >= 0; --k) {
+        for (int k = top; k >= 0; --k) {
             ECO_CUDA(cudaStreamWaitEvent(ovs, lvl_ev[k], 0));
             to_external_levels_kernel<Real><<<grid_for(ns), 256, 0, ovs>>>(d_J.p + (size_t)k * LV,
                                                                            d_tmp.p + (size_t)k * ns, ns, 1,
@@ -1095,12 +1098,12 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
                          std::chrono::duration<double, std::milli>(h2 - h1).count());
         }
     } else {
-        to_external_levels_kernel<Real><<<grid_for(ns * (H + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, H + 1,
-                                                                               pr->j_inf);
+        to_external_levels_kernel<Real><<<grid_for(ns * (top + 1)), 256, 0, st>>>(d_J.p, d_tmp.p, ns, top + 1,
+                                                                                 pr->j_inf);
         ECO_CUDA(cudaGetLastError());
         ++launches;
         all.stop(st);
-        download_big(J_stack, d_tmp.p, ns * (H + 1) * sizeof(double), st);
+        download_big(J_stack, d_tmp.p, ns * (top + 1) * sizeof(double), st);
         download_big(P_stack, d_P.p, ns * H * sizeof(int32_t), st);
     }
     unsigned long long live = 0;
@@ -2486,17 +2489,15 @@ int32_t eco_bellman_step(const EcoPlant* plant, const EcoProblem* prob, const Ec
         check_plant(plant);
         check_problem(prob);
         if (!plan || !J_next || !J_out || !P_out) throw ArgError{"null pointer argument"};
-        const size_t ns = (size_t)prob->n_v * prob->n_soc * prob->n_t;
         const bool rev = (precision & ECO_REVERSE_TIES) != 0;
         precision &= ~ECO_REVERSE_TIES;
-        std::vector<double> stack(2 * ns);
+        // level 0 straight into the caller's J_out (the terminal level is J_next)
         if (precision == ECO_FP64)
-            solve_horizon_impl<double>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats,
-                                       rev);
+            solve_horizon_impl<double>(plant, prob, plan, 1, tables, J_next, J_out, P_out, count_live, stats, rev,
+                                       true);
         else
-            solve_horizon_impl<float>(plant, prob, plan, 1, tables, J_next, stack.data(), P_out, count_live, stats,
-                                      rev);
-        std::memcpy(J_out, stack.data(), ns * sizeof(double));
+            solve_horizon_impl<float>(plant, prob, plan, 1, tables, J_next, J_out, P_out, count_live, stats, rev,
+                                      true);
     });
 }
 

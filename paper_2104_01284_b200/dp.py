@@ -396,8 +396,9 @@ def backward_step(ctx: SolveContext, k: int, J_next: np.ndarray, *, backend: str
     J_next = _f64(J_next)
     if J_next.shape != (g.n_v, g.n_soc, g.n_t):
         raise ValueError("J_next shape does not match the grid")
-    J_out = np.empty_like(J_next)
-    P_out = np.empty(J_next.shape, dtype=np.int32)
+    # page-locked outputs (recycled): direct DMA / host widening
+    J_out = _abi.PINNED.array(J_next.shape, np.float64)
+    P_out = _abi.PINNED.array(J_next.shape, np.int32)
     st = _abi.EcoStats()
     _abi.check(_abi.lib().eco_bellman_step(
         C.byref(m.plant), C.byref(m.prob), m.plans, None, _abi.ptr(J_next, C.c_double),

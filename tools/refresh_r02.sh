@@ -13,6 +13,7 @@ python bench.py --workload c2 > $O/${R}_bench_c2.json 2> $O/${R}_bench_c2.err; t
 python bench.py --workload c4 > $O/${R}_bench_c4.json 2> $O/${R}_bench_c4.err; tail -c 200 $O/${R}_bench_c4.json
 python bench.py --workload c5 --no-cpu-baseline > $O/${R}_bench_c5.json 2> $O/${R}_bench_c5.err; tail -c 200 $O/${R}_bench_c5.json
 python bench.py --workload n1 --steps 2 --warmup 1 --loop-steps 20 > $O/${R}_bench_n1.json 2> $O/${R}_bench_n1.err; tail -c 200 $O/${R}_bench_n1.json
+timeout 1500 python tools/reference_table1.py 10 $O/${R}_reference_table1.txt > /dev/null 2>&1; tail -2 $O/${R}_reference_table1.txt
 # launch lists (cold, serialised: shares, not absolutes)
 python tools/c3_probe.py --horizon 20 --reps 2 --no-count > /dev/null 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${R}_launches_c3.csv \
