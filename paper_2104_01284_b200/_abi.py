@@ -341,7 +341,11 @@ class PinnedPool:
         if blk is None:
             cap = (need + (2 << 20) - 1) & ~((2 << 20) - 1)
             out = C.c_void_p()
-            check(lib().eco_host_alloc(cap, C.byref(out)), "eco_host_alloc")
+            if lib().eco_host_alloc(cap, C.byref(out)) != OK or not out.value:
+                # host memory could not be page-locked (or there is no
+                # device, which the solver call reports): an ordinary array;
+                # the library then copies through its pinned staging
+                return np.empty(shape, dtype)
             blk = (cap, out.value)
         return np.asarray(_PinnedBuf(self, blk[1], blk[0], shape, dtype))
 
