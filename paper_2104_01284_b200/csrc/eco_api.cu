@@ -608,8 +608,8 @@ TileCfg tile_cfg(const Geometry<Real>& G, int nt, int mode, bool alias = false) 
         t.slices = std::max(1, std::min(env_int("ECO_TILE_SLICES", sl_default), std::max(1, 256 / t.S)));
         t.count_max = std::max(1, G.h_gmax[0]);
         t.band_cap = G.band_cap;
-        t.alias = alias ? 1 : 0;
-        t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, t.band_cap, alias).total;
+        t.alias = (alias || env_int("ECO_STAGE_ALIAS", 0) != 0) ? 1 : 0;
+        t.smem = TileSmem<Real>(nt, t.tj, t.slices, t.count_max, t.band_cap, t.alias != 0).total;
     }
     if (t.smem > 227 * 1024) throw ArgError{"tile reduction buffers exceed shared memory"};
     return t;
@@ -687,8 +687,11 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
             k = w2 ? bellman_wide2_kernel<Real, false, false, true>
                    : tc.wide ? bellman_wide_kernel<Real, false, false, true> : bellman_stage_kernel<Real, false, false, true>;
         } else if (w2) {
+            const bool fine = a.nt == kW2FineNT && env_int("ECO_W2_NTC", 1) != 0;
             k = a.npeer > 0 ? (count ? bellman_wide2_kernel<Real, true, true> : bellman_wide2_kernel<Real, false, true>)
-                            : (count ? bellman_wide2_kernel<Real, true> : bellman_wide2_kernel<Real, false>);
+                            : (count ? bellman_wide2_kernel<Real, true>
+                                     : fine ? bellman_wide2_kernel<Real, false, false, false, kW2FineNT>
+                                            : bellman_wide2_kernel<Real, false>);
         } else if (a.npeer > 0)
             k = tc.wide ? (count ? bellman_wide_kernel<Real, true, true> : bellman_wide_kernel<Real, false, true>)
                         : (count ? bellman_stage_kernel<Real, true, true> : bellman_stage_kernel<Real, false, true>);
@@ -1042,7 +1045,16 @@ void solve_horizon_impl(const EcoPlant* plant, const EcoProblem* pr, const EcoSt
             const int nb = nv * tc.nchunk;
             unsigned long long t0 = ~0ull, t1 = 0;
             for (int b = 0; b < nb; ++b) { t0 = std::min(t0, h[6 * b]); t1 = std::max(t1, h[6 * b + 3]); }
-            std::fprintf(stderr, "stage k=%d ctas=%d span=%.2fus\n", k, nb, (t1 - t0) / 1e3);
+            int cta_per_sm = 0;
+            if (tc.wide && w2_wpr(nt))
+                ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cta_per_sm, bellman_wide2_kernel<Real, false>,
+                                                                       tc.S * tc.slices, tc.smem));
+            else if (!tc.wide)
+                ECO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cta_per_sm, bellman_stage_kernel<Real, false>,
+                                                                       tc.S * tc.slices, tc.smem));
+            std::fprintf(stderr, "stage k=%d ctas=%d span=%.2fus tile %dx%d slices %d count_max %d band_cap %d smem %zu "
+                         "ctas/SM %d\n", k, nb, (t1 - t0) / 1e3, tc.tj, nt, tc.slices, tc.count_max, tc.band_cap,
+                         tc.smem, cta_per_sm);
             for (int b = 0; b < nb; ++b)
                 std::fprintf(stderr, "  cta %3d sm %3llu path %llu work %5llu start %7.2f staged %7.2f looped %7.2f end %7.2f\n",
                              b, h[6 * b + 4] & 0xFFFF, h[6 * b + 4] >> 16, h[6 * b + 5], (h[6 * b] - t0) / 1e3,

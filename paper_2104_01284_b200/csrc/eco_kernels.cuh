@@ -792,13 +792,17 @@ __device__ __forceinline__ bool improves(Real F, Real best) {
 #define ECO_W2R 4
 #endif
 constexpr int kW2R = ECO_W2R;  // source rows per warp (= per CTA)
-constexpr int kW2S = 63;       // ladder states per warp: 64 samples (2 per lane), the last state
-                               // dropped (its t' + 1 sample sits in the next warp's range)
+constexpr int kW2S = 62;       // ladder states per warp: 64 samples (2 per lane); lane 31's two
+                               // states are dropped (the t' + 1 sample of the last one sits in the
+                               // next warp's range), so every warp starts on an even state
 
-// Per (tile, action) summary built in the CTA prologue: base = the (ivlo,
-// jxlo, zoff) index of row 0 when the fast path applies (all kW2R rows on the
-// hull, consecutive destination rows, non-degenerate SoC and speed cells),
-// else -1; wx = the rows' SoC weights.  Kept in the tile's (unused) band region.
+// Per (tile, action) summary built in the CTA prologue: base = where row 0's
+// (ivlo, jxlo, zoff) corner pair lives when the fast path applies (all kW2R
+// rows on the hull, consecutive destination rows, non-degenerate SoC and
+// speed cells), else -1: the even index below it in copy 0 of J_{k+1}, or in
+// copy 1 (at + lc) for an odd index -- warps start on even states, so one
+// resolved offset serves them all; wx = the rows' SoC weights.  Kept in the
+// tile's (unused) band region.
 template <typename Real>
 struct alignas(8) W2Quad {
     int32_t base, zl;          // zl: last live ladder state of the action's rows (n_t - 1 - zoff - dzh)
@@ -807,7 +811,7 @@ struct alignas(8) W2Quad {
 
 // One warp's action scan over its kW2R rows x kW2S states (W2).  best / bk
 // index r * 2 + i.  RED: the stage has red arrival samples.
-template <typename Real, bool COUNT, bool REV, bool RED>
+template <typename Real, bool COUNT, bool REV, bool RED, int NTC = 0>
 __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<Real>* __restrict__ s_ro,
                                         const ActRec<Real>* __restrict__ s_act, const W2Quad<Real>* __restrict__ s_q,
                                         const uint8_t* __restrict__ s_green, int count, int nr, int zs,
@@ -816,11 +820,14 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
     using V2 = typename Vec2<Real>::T;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int nt = a.nt, plane = a.nx * nt, tj = a.tj;
+    // NTC > 0: the ladder length as a compile-time constant (the fine-grid
+    // instantiation): the corner rows' offsets become load immediates
+    const int nt = NTC > 0 ? NTC : a.nt, plane = a.nx * nt, tj = a.tj;
     const int z0 = zs + 2 * lane;                            // the lane's two states z0, z0 + 1
-    const bool keep1 = lane != 31;                           // state zs + 63: next warp's t' + 1 sample
+    const bool keep1 = lane != 31;                           // lane 31's states belong to the next warp
     const Real* __restrict__ J0 = a.J_next;
     const Real* __restrict__ J1 = a.J_next1;
+    const Real* __restrict__ Jw = J0 + z0;                   // + a resolved W2Quad::base
     for (int k = 0; k < count; ++k) {
         const W2Quad<Real> qd = s_q[k];
         const int zl = qd.zl;                                // last live state of every valid row
@@ -830,8 +837,9 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
         const bool dzh = (rc.meta & kRecDzh) != 0;
         const bool gated = RED && (rc.meta & kRecGated) != 0;
         const Real wv = rc.wv, wz = rc.wz, c1 = rc.c1;
+        // (lane 31's results are never stored: no mask needed for them)
         const bool ok0 = z0 <= zl && (!gated || s_green[min(z0 + zoff, nt - 1)] != 0);           // K:516
-        const bool ok1 = keep1 && z0 + 1 <= zl && (!gated || s_green[min(z0 + 1 + zoff, nt - 1)] != 0);
+        const bool ok1 = z0 + 1 <= zl && (!gated || s_green[min(z0 + 1 + zoff, nt - 1)] != 0);
         // t-blend (K:361) of the SoC-blended pair + lexicographic update; the
         // pair's second state takes its t' + 1 sample from the next lane
         auto update = [&](int r, PR col) {
@@ -842,7 +850,7 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
             const PR nb{dzh ? col.y : col.x, dzh ? nxt : col.y};
             PR f = p_lerp(col, nb, wz);
             f = p_addc(f, c1);
-            if (COUNT) nlive += ok0 + ok1;
+            if (COUNT) nlive += keep1 ? ok0 + ok1 : 0;
             const bool u0 = ok0 && improves<REV>(f.x, best[2 * r]);
             const bool u1 = ok1 && improves<REV>(f.y, best[2 * r + 1]);
             best[2 * r] = u0 ? f.x : best[2 * r];
@@ -854,14 +862,14 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
             // kW2R + 1 consecutive destination rows, speed-blended once and
             // shared by the kW2R source rows (the reference's lerp tree:
             // v inside, then SoC, K:335-337)
-            const unsigned base = (unsigned)(qd.base + zs);
-            const Real* p = ((base & 1u) ? J1 : J0) + (base & ~1u) + 2 * lane;
+            const Real* p = Jw + qd.base;
+            const Real* ph = p + plane;                      // the upper speed corner's rows
             V2 tl[kW2R + 1], th[kW2R + 1];
             if (!ECO_CHK_IN(p, kW2R * nt + plane + 2, J0, 2 * a.lc)) continue;
 #pragma unroll
             for (int q = 0; q <= kW2R; ++q) {
                 tl[q] = __ldg(reinterpret_cast<const V2*>(p + q * nt));
-                th[q] = __ldg(reinterpret_cast<const V2*>(p + q * nt + plane));
+                th[q] = __ldg(reinterpret_cast<const V2*>(ph + q * nt));
             }
             PR vb[kW2R + 1];
 #pragma unroll
@@ -894,7 +902,7 @@ __device__ __forceinline__ void w2_scan(const StageArgs<Real>& a, const RowRec<R
 }
 
 template <typename Real, bool COUNT, bool WIDE = false, bool PEERS = false, bool PREFETCH = false, bool REV = false,
-          bool W2 = false>
+          bool W2 = false, int NTC = 0>
 __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int rank, unsigned char* smem) {
     using V2 = typename Vec2<Real>::T;
     unsigned long long* dbg = a.dbg ? a.dbg + 6 * rank : nullptr;
@@ -1178,7 +1186,9 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
                 q.wx[r] = ro.wx;
                 f = f && ro.wx > (Real)0 && ro.off == rk[0].off + r * nt;
             }
-            q.base = f ? rk[0].off : -1;
+            // (levels whose two copies exceed int32 indexing take the per-row path)
+            f = f && 2 * a.lc + (size_t)plane < (size_t)INT32_MAX;
+            q.base = f ? (rk[0].off & ~1) + ((rk[0].off & 1) ? (int32_t)a.lc : 0) : -1;
             const uint32_t m = s_act[k].meta;
             q.zl = nt - 1 - (int)(m & kRecZoff) - ((m & kRecDzh) ? 1 : 0);
             s_q[k] = q;
@@ -1195,8 +1205,8 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
 #pragma unroll
         for (int i = 0; i < 2 * kW2R; ++i) { best[i] = a.j_inf; bk[i] = -1; }
         if (zs < nt) {
-            if (any_red) w2_scan<Real, COUNT, REV, true>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
-            else w2_scan<Real, COUNT, REV, false>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
+            if (any_red) w2_scan<Real, COUNT, REV, true, NTC>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
+            else w2_scan<Real, COUNT, REV, false, NTC>(a, s_ro, s_act, s_q, s_green, count, nr, zs, best, bk, nlive);
         }
         // results straight from registers: every state has one owner thread
         if (COUNT && a.live) {
@@ -1556,11 +1566,15 @@ __device__ __forceinline__ void stage_tile(const StageArgs<Real>& a, const int r
         Real best = (Real)INFINITY;
         int bk = -1;
         if (live) {
+            // unrolled, unconditional loads: the slices' shared-memory reads
+            // issue back to back instead of one dependent round trip each
+#pragma unroll 4
             for (int s = s0; s < s1; ++s) {
                 const int k2 = s_arg[s * tj_nt + f];
-                if (k2 < 0) continue;
                 const Real b2 = s_best[s * tj_nt + f];
-                if (bk < 0 || b2 < best || (b2 == best && (REV ? k2 > bk : k2 < bk))) { best = b2; bk = k2; }
+                const bool take = k2 >= 0 && (bk < 0 || b2 < best || (b2 == best && (REV ? k2 > bk : k2 < bk)));
+                best = take ? b2 : best;
+                bk = take ? k2 : bk;
             }
         }
         if (pair) {
@@ -1615,13 +1629,16 @@ bellman_wide_kernel(StageArgs<Real> a) {
 #ifndef ECO_W2_MINB
 #define ECO_W2_MINB 4
 #endif
-constexpr int kW2MaxWarps = 7;   // n_t <= 7 * kW2S = 441 (longer ladders: bellman_wide_kernel)
-template <typename Real, bool COUNT, bool PEERS = false, bool REV = false>
+constexpr int kW2MaxWarps = 7;   // n_t <= 7 * kW2S = 434 (longer ladders: bellman_wide_kernel)
+// ladder length compiled into a dedicated instantiation (the fine grids'
+// 80 s / 0.2 s ladder); every other length runs the runtime-n_t kernel
+constexpr int kW2FineNT = 400;
+template <typename Real, bool COUNT, bool PEERS = false, bool REV = false, int NTC = 0>
 __global__ void __launch_bounds__(32 * kW2MaxWarps, ECO_W2_MINB)
 bellman_wide2_kernel(StageArgs<Real> a) {
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem[];
-    stage_tile<Real, COUNT, true, PEERS, false, REV, true>(a, blockIdx.x, smem);
+    stage_tile<Real, COUNT, true, PEERS, false, REV, true, NTC>(a, blockIdx.x, smem);
 }
 
 // Single-GPU emulation of a G-rank slab stage (tests of the C5 exchange on a
