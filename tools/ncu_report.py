@@ -40,7 +40,7 @@ for name, label, scale in (("lts__t_bytes.sum", "L2 traffic", 1), ("lts__t_secto
                            ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 reads from the SMs", 32),
                            ("l1tex__t_bytes.sum", "L1 traffic", 1),
                            ("SM_B.TriageCompute.l1tex__t_sectors.sum", "L1 traffic", 32)):
-    if name in d:
+    if name in d and d[name][0] != "no data":
         b = num(name)[0] * scale
         lines.append(f"{label} ({name}): {b / 1e9:.1f} GB per launch = {b / dur / 1e12:.2f} TB/s")
 for name in ("lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
