@@ -542,12 +542,14 @@ def test_session_route_reupload_matches_fresh_session(vehicle):
     with_fresh.close(); reused.close()
 
 
-@pytest.mark.parametrize("nt", [128, 129, 130, 192, 256, 258, 322, 512])
+@pytest.mark.parametrize("nt", [128, 129, 130, 192, 256, 258, 322, 400, 434, 435, 512])
 def test_wide_row_path_vs_oracle(vehicle, urban_route, nt):
-    """Long ladders take the wide-row kernel: odd chunk counts, partial last
-    chunks, ranges that end exactly on / one past a warp segment; fp64
-    bitwise against the oracle, fp32 within tolerance (incl. the signal at
-    node 80 inside the horizon: red gates, standstill relocation)."""
+    """Long ladders take the wide-row kernels: odd chunk counts, partial last
+    chunks, ranges that end exactly on / one past a warp segment, the
+    compiled n_t = 400 instantiation, the longest row-block ladder (7 warps x
+    62 states = 434) and the first one past it; fp64 bitwise against the
+    oracle, fp32 within tolerance (incl. the signal at node 80 inside the
+    horizon: red gates, standstill relocation)."""
     route, spat = urban_route
     grids = GridSpec(n_v=7, n_soc=5, n_t=nt, dt=0.25)
     for s, t in [(62, 31.0), (76, 5.5)]:
@@ -637,6 +639,19 @@ def test_closed_loop_variants_fp32_within_0p1pct(vehicle, kind, seed, gamma):
     fuel_ref = float(np.sum(ref["rows"]["fuel_inc_g"]))
     assert abs(traj.fuel_g - fuel_ref) <= 1e-3 * fuel_ref, (traj.fuel_g, fuel_ref)
     assert abs(traj.final_state.t - ref["final"][2]) <= 1e-3 * ref["final"][2], (traj.final_state.t, ref["final"][2])
+
+
+def test_c3_compiled_ladder_equals_runtime_ladder(c3_short_ctx, monkeypatch):
+    """The n_t = 400 instantiation of the row-block kernel (compile-time
+    ladder length) and the runtime-n_t kernel (ECO_W2_NTC=0) give the same
+    tables and policies bit for bit, fp64 and fp32."""
+    from paper_2104_01284_b200.dp import solve_stacks
+    for backend in ("b200-fp64", "b200"):
+        monkeypatch.delenv("ECO_W2_NTC", raising=False)
+        J1, P1, _ = solve_stacks(c3_short_ctx, backend)
+        monkeypatch.setenv("ECO_W2_NTC", "0")
+        J0, P0, _ = solve_stacks(c3_short_ctx, backend)
+        assert np.array_equal(J1, J0) and np.array_equal(P1, P0), backend
 
 
 def test_c3_host_widened_levels_equal_device_conversion(c3_short_ctx, monkeypatch):
