@@ -787,9 +787,10 @@ __device__ __forceinline__ bool improves(Real F, Real best) {
 // (no slice merge).  For one action the kW2R rows land on consecutive
 // destination rows (xi' = xi - dt*I/C_nom shifts every row alike: checked per
 // action, else a per-row path), so kW2R + 1 destination rows per speed corner
-// serve all kW2R source rows from registers: 10 row loads instead of 16.
+// serve all kW2R source rows from registers: 12 row loads instead of 20
+// (5 rows: 260 SoC rows = 52 whole blocks; measured 3 % faster than 4).
 #ifndef ECO_W2R
-#define ECO_W2R 4
+#define ECO_W2R 5
 #endif
 constexpr int kW2R = ECO_W2R;  // source rows per warp (= per CTA)
 constexpr int kW2S = 62;       // ladder states per warp: 64 samples (2 per lane); lane 31's two
