@@ -610,7 +610,7 @@ def run_c3(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(21 * ns * (4 if args.precision == "fp32" else 8) + 20 * ns * 4),
                 "api": "paper_2104_01284_b200.solve_horizon(ctx, backend) -> SolveResult with all 21 f64 J and "
                        "20 int32 P levels on the host (9.0 GB; pinned output pool)"},
-        "roofline": _roofline(args, local_rank, live, sweep_max / args.steps / 1e3, "bellman_wide_kernel",
+        "roofline": _roofline(args, local_rank, live, sweep_max / args.steps / 1e3, "bellman_wide2_kernel",
                               traffic, tsrc, algorithmic_bytes=ns * 4 + 3 * ns * 4),
         "clocks": clk.summary(),
     }
@@ -783,7 +783,7 @@ def run_c5(args, rank, world, local_rank):
         "e2e": {"value": dense * args.steps / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
                 "h2d_bytes_per_step": int(ns * 8), "d2h_bytes_per_step": int(res.P.nbytes)},
         "roofline": _roofline(args, local_rank, live_all / world, sweep_max / args.steps / 1e3,
-                              "bellman_wide_kernel", *measured_traffic(f"c5_{args.precision}")),
+                              "bellman_wide2_kernel", *measured_traffic(f"c5_{args.precision}")),
         "clocks": clk.summary(),
     }
     if dist is not None:
@@ -850,7 +850,7 @@ def run_n1(args, rank, world, local_rank):
         "ms_per_solve": t_max / args.steps / M, "sweep_ms_per_solve": sweep_ms / args.steps / M,
         "live_updates_per_step": live, "gpu_launches": int(launches),
         "final_state": [float(x) for x in fin],
-        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_wide_kernel",
+        "roofline": _roofline(args, local_rank, live, sweep_ms / args.steps / 1e3, "bellman_wide2_kernel",
                               *measured_traffic(f"c3_{args.precision}")),
         "clocks": clk.summary(),
     }
