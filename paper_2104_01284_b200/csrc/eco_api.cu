@@ -486,7 +486,7 @@ void build_geometry(Geometry<Real>& G, const EcoPlant* d_plant, const DevPlan* d
     if (G.row.cap < (size_t)std::max<int64_t>(1, G.rows_total)) G.row.alloc((size_t)std::max<int64_t>(1, G.rows_total));
     const size_t smem = (size_t)g.ntb * g.nx * (sizeof(double) + 1) + 16;
     set_smem_attr(geom_soc_kernel<Real>, smem);
-    geom_soc_kernel<Real><<<grid, 256, smem, st>>>(d_plant, d_vaxes, d_tb, d_soc, g, G.view(),
+    geom_soc_kernel<Real><<<grid, ECO_SOC_THREADS, smem, st>>>(d_plant, d_vaxes, d_tb, d_soc, g, G.view(),
                                                    d_tab.ok != nullptr ? 1 : 0);
     ECO_CUDA(cudaGetLastError());
     geom_unpack_u_kernel<<<npi, 256, 0, st>>>(G.u.p, G.count.p, g.U);

@@ -174,8 +174,11 @@ __global__ void geom_rowoff_kernel(const int32_t* __restrict__ count, int64_t* _
 // then xi' = xi - dt*I/C_nom and its cell (K:498-506 / K:709-712) for every
 // compacted pair -> RowRec.  grid (nv, P), block 256; per_action_pbat = toy
 // mode (K:676-683).
+#ifndef ECO_SOC_THREADS
+#define ECO_SOC_THREADS 512
+#endif
 template <typename Real>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(ECO_SOC_THREADS)
 geom_soc_kernel(const EcoPlant* __restrict__ plant, const double* __restrict__ vaxes,
                 const double* __restrict__ tb_axis, const double* __restrict__ soc_axis, GeomDims g,
                 PairGeom<Real> out, int per_action_pbat) {
