@@ -688,7 +688,9 @@ void launch_stage(const StageArgs<Real>& a, const TileCfg& tc, bool count, cudaS
                    : tc.wide ? bellman_wide_kernel<Real, false, false, true> : bellman_stage_kernel<Real, false, false, true>;
         } else if (w2) {
             const bool fine = a.nt == kW2FineNT && env_int("ECO_W2_NTC", 1) != 0;
-            k = a.npeer > 0 ? (count ? bellman_wide2_kernel<Real, true, true> : bellman_wide2_kernel<Real, false, true>)
+            k = a.npeer > 0 ? (count ? bellman_wide2_kernel<Real, true, true>
+                                     : fine ? bellman_wide2_kernel<Real, false, true, false, kW2FineNT>
+                                            : bellman_wide2_kernel<Real, false, true>)
                             : (count ? bellman_wide2_kernel<Real, true>
                                      : fine ? bellman_wide2_kernel<Real, false, false, false, kW2FineNT>
                                             : bellman_wide2_kernel<Real, false>);
