@@ -1869,7 +1869,7 @@ struct Batch : BatchBase {
     bool fitted = false;
     size_t cap = 0;                       // scenarios the per-chunk buffers hold
     DBuf<EcoSignalTiming> tim;
-    DBuf<int32_t> s_d, h_d, P0_d[2];
+    DBuf<int32_t> s_d, h_d, ord_d, P0_d[2];
     DBuf<double> t_d, tdep, wait, tax, J0_d[2];
     cudaStream_t st_out = 0;       // D2H of chunk c overlaps the compute of chunk c + 1
     cudaEvent_t ev_out[2]{};
@@ -1920,7 +1920,7 @@ struct Batch : BatchBase {
         if (B <= cap) return;
         const int nt = cfg.n_t;
         tim.alloc(B * std::max(1, n_sig));
-        s_d.alloc(B); h_d.alloc(B); t_d.alloc(B);
+        s_d.alloc(B); h_d.alloc(B); t_d.alloc(B); ord_d.alloc(B);
         green.alloc(B * (H + 1) * nt); dep.alloc(B * (H + 1) * nt);
         tdep.alloc(B * (H + 1) * nt); wait.alloc(B * (H + 1) * nt); tax.alloc(B * nt);
         bflags.alloc(B * H);
@@ -1999,6 +1999,12 @@ struct Batch : BatchBase {
             s_d.upload(s_h + c0, B, st);
             t_d.upload(t_h + c0, B, st);
             h_d.upload(hh.data(), B, st);
+            // launch order of the scenarios: by start node (stable)
+            std::vector<int32_t> ord(B);
+            for (int i = 0; i < B; ++i) ord[i] = i;
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return s_h[c0 + x] < s_h[c0 + y]; });
+            const bool sorted = env_int("ECO_BATCH_SORT", 1) != 0;
+            if (sorted) ord_d.upload(ord.data(), B, st);
             if (n_sig) tim.upload(tim_h + (size_t)c0 * n_sig, (size_t)B * n_sig, st);
             const unsigned pblocks = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (ns + 255) / 256));
             batch_prepare_kernel<Real><<<dim3(pblocks, B), 256, 0, st>>>(
@@ -2019,6 +2025,7 @@ struct Batch : BatchBase {
             ba.green = green.p; ba.dep_ok = dep.p; ba.t_dep = tdep.p; ba.wait = wait.p; ba.t_axis = tax.p;
             ba.flags = bflags.p;
             ba.J = J.p; ba.LV = LV; ba.LC = LC;
+            ba.order = sorted ? ord_d.p : nullptr;
             if (P0 && P0_d[ob].n < (size_t)B * ns) P0_d[ob].alloc((size_t)std::min(chunk, n_scen) * ns);
             ba.P0 = P0 ? P0_d[ob].p : nullptr;
             sw.start(st);

@@ -1703,13 +1703,16 @@ struct BatchArgs {
     Real* J;                      // [B][2] levels of LV elements (copy 0 at +0, copy 1 at +LC)
     size_t LV, LC;
     int32_t* P0;                  // [B][nv*nx*nt] or nullptr
+    const int32_t* order;         // [B] scenario of grid row y (by start node, nullable)
 };
 
 template <typename Real, bool COUNT>
 __global__ void __launch_bounds__(512)
 bellman_batch_kernel(BatchArgs<Real> ba) {
     pdl_launch_dependents();
-    const int b = blockIdx.y, k = ba.k;
+    // grid rows visit the scenarios by start node: neighbouring CTAs then use
+    // the same plans, whose row records stay in L2 between them
+    const int b = ba.order ? ba.order[blockIdx.y] : (int)blockIdx.y, k = ba.k;
     if (k >= ba.h[b]) return;
     extern __shared__ __align__(16) unsigned char smem[];
     StageArgs<Real> a = ba.base;
